@@ -1,0 +1,23 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: full-size configurations")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_host_libs():
+    # host-only C libraries (oracle, generators): gcc, seconds
+    import oracle
+    import workloads
+    oracle.build()
+    workloads.build()
+    yield
