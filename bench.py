@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the SpTRSV hot path (arXiv 1710.04985) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--algo self]
+                [--impl ours|reference]
+
+A step is one solve of the configuration's triangular system(s) on an
+analyzed handle (the setup phase is timed separately, as in the paper's
+Tables 4-6, and reported as config.analysis_ms).  Inputs are seeded synthetic
+matrices of the paper's workload shapes (workloads/).  Timing: W >= 3 warm-up
+steps, then exactly K steps between barrier + synchronize; each solve is
+bracketed by CUDA events on the launching stream and the L2 is flushed (a
+256 MiB write, outside the events) before every timed solve.  Multi-GPU:
+one process per GPU (torchrun), each rank solves its own independent RHS
+(weak scaling; config 5 partitions 64 RHS, strong scaling), the time is the
+max over ranks.
+
+Metric (BASELINE.json): effective HBM GB/s per solve = compulsory bytes /
+time, bytes = 4(n+1) + (4+s)nnz(T) + 2 s n nrhs; GFLOP/s
+= nrhs (2 #offdiag + n_div) / time is reported beside it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0          # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+NOMINAL_HBM_GBS = 8000.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--algo", default="self", choices=["self", "level", "block"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--extra", action="store_true", help="also time the other algos and print them")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+def build_problem(cfg: int, rank: int, world: int):
+    """Matrix + RHS of a configuration (identical on every rank: seeded).
+    Returns dict with the CSR, solve list [(uplo, diag)], rhs and work counts."""
+    import workloads
+    m, p = workloads.config(cfg)
+    if cfg == 3:
+        solves = [("lower", "unit"), ("upper", "non_unit")]
+    else:
+        solves = [(p["uplo"], p["diag"])]
+    if cfg == 5:
+        from paper_1710_04985_b200 import partition
+        a, b = partition.block_range(64, world, rank)
+        rhs = workloads.rhs_columns(m.n, range(a, b))
+        scaling = "strong"
+    else:
+        rhs = workloads.rhs(m.n, 1, seed=p["seed"] + 7919 * rank)
+        scaling = "weak"
+    return {"m": m, "solves": solves, "rhs": rhs, "scaling": scaling, "params": p}
+
+
+def work_counts(m, solves, nrhs, esize):
+    """Compulsory bytes and flops of one step (reading Q13)."""
+    import oracle
+    nbytes = 0
+    flops = 0
+    for uplo, diag in solves:
+        sel = oracle.select(m, uplo, diag)
+        offd = sel["nnz_used"]
+        nnz_t = offd + (m.n if diag == "non_unit" else 0)
+        nbytes += 4 * (m.n + 1) + (4 + esize) * nnz_t + 2 * esize * m.n * nrhs
+        flops += nrhs * (2 * offd + (m.n if diag == "non_unit" else 0))
+    return nbytes, flops
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(key):
+    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def time_oracle(m, solves, rhs, budget_s, min_reps=1, max_reps=None):
+    """Repeat the oracle's full solves (the whole workload, single-threaded C)
+    until ``budget_s`` seconds of CPU work; returns (seconds per step, reps)."""
+    import oracle
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        z = rhs
+        for uplo, diag in solves:
+            z = oracle.solve(m, z, uplo, diag)
+        reps += 1
+        el = time.perf_counter() - t0
+        if (el >= budget_s and reps >= min_reps) or (max_reps and reps >= max_reps):
+            break
+    return el / reps, reps
+
+
+def run_reference(args):
+    """--impl reference: this tier's reference arm is the CPU oracle as it
+    stands, timed on the host cores on the same config/metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    prob = build_problem(args.config, 0, 1)
+    m, solves, rhs = prob["m"], prob["solves"], prob["rhs"]
+    esize = 8 if args.dtype == "f64" else 4
+    nbytes, flops = work_counts(m, solves, rhs.shape[1], esize)
+    # warmup W untimed steps, then K timed steps (each = the full solve, bounded by the workload)
+    for _ in range(args.warmup):
+        time_oracle(m, solves, rhs, 0.0, max_reps=1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time_oracle(m, solves, rhs, 0.0, max_reps=1)
+    per = (time.perf_counter() - t0) / max(1, args.steps)
+    value = nbytes / per / 1e9
+    line = {
+        "impl": "reference", "metric": "SpTRSV effective HBM GB/s per solve (fraction of B200 peak)",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(per * 1e3, 4), "higher_is_better": True,
+        "scaling": prob["scaling"], "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "gflops": round(flops / per / 1e9, 4),
+        "config": {"workload": config_name(args.config), "n": m.n, "nrhs": int(rhs.shape[1]),
+                   "bytes_per_step": nbytes, "flops_per_step": flops},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} full oracle solves of {config_name(args.config)}"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_name(cfg):
+    return {1: "cfg1: L+D of 2D 5-point 32x32, fp64, 1 RHS",
+            2: "cfg2: L+D of 3D 7-point 128^3 (n=2097152), fp64, 1 RHS",
+            3: "cfg3: ILU(0) of 3D 27-point 96^3, forward (unit L) + backward (U) solve, fp64",
+            4: "cfg4: generated power-law lower factor n=4194304 nlev=12288, fp64",
+            5: "cfg5: 64 RHS on the 3D 7-point 128^3 factor, column-partitioned over ranks"}[cfg]
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1710_04985_b200 import sptrsv as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    prob = build_problem(args.config, rank, world)
+    m, solves, rhs_np = prob["m"], prob["solves"], prob["rhs"]
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    esize = 8 if args.dtype == "f64" else 4
+    nrhs = rhs_np.shape[1]
+    nbytes, flops = work_counts(m, solves, nrhs, esize)
+
+    stream = torch.cuda.current_stream()
+    t_an = time.perf_counter()
+    handles = [S.from_csr(m, uplo, diag, dtype=dt, algo=args.algo) for uplo, diag in solves]
+    torch.cuda.synchronize()
+    analysis_ms = (time.perf_counter() - t_an) * 1e3
+    an_infos = [h.info() for h in handles]
+
+    b = torch.from_numpy(np.ascontiguousarray(rhs_np[:, 0] if nrhs == 1 else rhs_np)).to(dev, dt)
+    bufs = [torch.empty_like(b) for _ in handles]
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        z = b
+        for h, out in zip(handles, bufs):
+            h.solve(z, out)
+            z = out
+        return z
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # correctness guard on the timed configuration (sampled; the tests do full parity)
+    times = []
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    times = np.array([a.elapsed_time(e) for a, e in ev]) / 1e3          # seconds per step
+    t_mean = float(times.mean())
+    t_med = float(np.median(times))
+    if world > 1:
+        tt = torch.tensor([t_mean], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    else:
+        t_max = t_mean
+    total_bytes = nbytes * (world if prob["scaling"] == "weak" else 1)
+    total_flops = flops * (world if prob["scaling"] == "weak" else 1)
+    if prob["scaling"] == "strong":
+        # config 5: bytes counted per GPU (each replica streams the matrix), summed
+        tb = torch.tensor([nbytes, flops], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tb)
+        total_bytes, total_flops = float(tb[0].item()), float(tb[1].item())
+    value = total_bytes / t_max / 1e9
+
+    # e2e through the C ABI with HOST buffers (pinned), H2D + D2H inside the region
+    e2e = None
+    if not args.no_e2e:
+        hb = torch.from_numpy(np.ascontiguousarray(rhs_np[:, 0] if nrhs == 1 else rhs_np)).to(dt).pin_memory()
+        hx = [torch.empty_like(hb).pin_memory() for _ in handles]
+        for _ in range(3):
+            z = hb
+            for h, out in zip(handles, hx):
+                h.solve_host(z, out)
+                z = out
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        k_e2e = max(5, min(args.steps, 20))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            z = hb
+            for h, out in zip(handles, hx):
+                h.solve_host(z, out)
+                z = out
+        t_e2e = (time.perf_counter() - t0) / k_e2e
+        if world > 1:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        e2e = {"value": round(total_bytes / t_e2e / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(hb.numel() * esize * len(handles)),
+               "d2h_bytes_per_step": int(hb.numel() * esize * len(handles)),
+               "ms_per_step": round(t_e2e * 1e3, 4), "api": "sptrsv_solve_host"}
+
+    # extra: the other algorithms on the same problem (context, rank 0 prints)
+    extra = {}
+    if args.extra and world == 1:
+        for algo in ("self", "level", "block"):
+            if algo == args.algo:
+                continue
+            try:
+                for h in handles:
+                    h.set_algo(algo)
+            except Exception as e:          # not available
+                extra[algo] = str(e)
+                continue
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(max(5, args.steps // 2)):
+                if flush is not None:
+                    flush.zero_()
+                a_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                step()
+                e_.record(stream)
+                e_.synchronize()
+                ts.append(a_.elapsed_time(e_) / 1e3)
+            tm = float(np.mean(ts))
+            extra[algo] = {"us_per_step": round(tm * 1e6, 2), "GB/s": round(nbytes / tm / 1e9, 2)}
+        for h in handles:
+            h.set_algo(args.algo)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peak()
+    achieved = nbytes / t_mean / 1e9     # per launch on this rank: bytes of one step / mean step time
+    launches_per_step = len(handles)
+    cpu = None
+    if not args.no_cpu and world == 1:
+        per, reps = time_oracle(m, solves, rhs_np, args.cpu_budget, min_reps=2)
+        cpu = {"value": round(nbytes / per / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{reps} full oracle solves of the same workload ({per * 1e3:.1f} ms each, "
+                         f"~{args.cpu_budget:.0f} s budget), single-threaded C -O2"}
+    key = f"cfg{args.config}_{args.algo}_{args.dtype}"
+    clk_s = clk.summary()
+    line = {
+        "metric": "SpTRSV effective HBM GB/s per solve (fraction of B200 peak)",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(t_max * 1e3, 5),
+        "higher_is_better": True, "scaling": prob["scaling"], "vs_baseline": None,
+        "dtype": args.dtype, "data": "synthetic (seeded generators, workloads/)",
+        "gflops": round(total_flops / t_max / 1e9, 3),
+        "config": {"workload": config_name(args.config), "algo": args.algo, "n": m.n, "nrhs": int(nrhs),
+                   "nnz_used": [i["nnz_used"] for i in an_infos], "nlev": [i["nlev"] for i in an_infos],
+                   "bytes_per_step": nbytes, "flops_per_step": flops,
+                   "analysis_ms": round(analysis_ms, 2),
+                   "l2": "flushed before every timed solve (256 MiB write)" if flush is not None else "warm",
+                   "median_us": round(t_med * 1e6, 2), "min_us": round(float(times.min()) * 1e6, 2),
+                   "parallelism": f"replicas{world}" if prob["scaling"] == "weak" else f"rhs-partition{world}"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(key), "peak_source": peak_src,
+                     "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
+                     "kernel": {"self": "k_self", "level": "k_level", "block": "k_block"}[args.algo]
+                     if nrhs == 1 else "k_mrhs"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(args.steps * launches_per_step),
+        "clocks": clk_s,
+    }
+    if extra:
+        line["extra_algos"] = extra
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

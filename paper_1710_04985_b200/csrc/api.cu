@@ -1,0 +1,206 @@
+// api.cu -- the C ABI of include/sptrsv.h: argument checks, handle lifecycle,
+// host staging.  All arithmetic runs in analyze.cu / solve.cu / block.cu.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+namespace sptrsv {
+
+static thread_local char g_last_cuda[256] = "";
+
+sptrsv_status_t cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_last_cuda, sizeof(g_last_cuda), "%s: %s", where, cudaGetErrorString(e));
+    if (e == cudaErrorMemoryAllocation) return SPTRSV_ERR_ALLOC;
+    return SPTRSV_ERR_CUDA;
+}
+
+sptrsv_status_t DevArena::alloc(void **p, size_t nbytes) {
+    *p = nullptr;
+    if (nbytes == 0) nbytes = 16;
+    cudaError_t e = cudaMalloc(p, nbytes);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        return cuda_fail(e, "cudaMalloc");
+    }
+    ptrs.push_back(*p);
+    bytes += (int64_t)nbytes;
+    return SPTRSV_SUCCESS;
+}
+
+void DevArena::release_all() {
+    for (void *p : ptrs) cudaFree(p);
+    ptrs.clear();
+    bytes = 0;
+}
+
+}  // namespace sptrsv
+
+using namespace sptrsv;
+
+static bool valid_enum(int v) { return v == 0 || v == 1; }
+
+extern "C" sptrsv_status_t sptrsv_analyze(int32_t n, const int32_t *rowptr, const int32_t *colidx,
+                                          const void *vals, sptrsv_uplo_t uplo, sptrsv_diag_t diag,
+                                          sptrsv_dtype_t dtype, sptrsv_stream_t stream,
+                                          sptrsv_handle_t *out) {
+    if (!out) return SPTRSV_ERR_INVALID_VALUE;
+    *out = nullptr;
+    if (n < 0 || !valid_enum(uplo) || !valid_enum(diag) || !valid_enum(dtype)) return SPTRSV_ERR_INVALID_VALUE;
+    if (n > 0 && (!rowptr || !colidx || (!vals && diag == SPTRSV_NON_UNIT))) return SPTRSV_ERR_INVALID_VALUE;
+
+    auto t0 = std::chrono::steady_clock::now();
+    int dev = 0;
+    SPTRSV_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    SPTRSV_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) return SPTRSV_ERR_NOT_SUPPORTED;
+
+    sptrsv_handle_t h = new (std::nothrow) sptrsv_handle_s();
+    if (!h) return SPTRSV_ERR_ALLOC;
+    h->n = n;
+    h->uplo = uplo;
+    h->diag = diag;
+    h->dtype = dtype;
+    h->device = dev;
+    h->num_sms = prop.multiProcessorCount;
+    h->esize = dtype == SPTRSV_F64 ? 8 : 4;
+    h->info.n = n;
+    h->info.uplo = uplo;
+    h->info.diag = diag;
+    h->info.dtype = dtype;
+    h->info.algo = SPTRSV_ALGO_SELF;
+    h->info.zero_pivot_row = -1;
+    h->info.bad_row = -1;
+
+    sptrsv_status_t st = SPTRSV_SUCCESS;
+    if (n > 0) st = analyze_impl(h, rowptr, colidx, vals, (cudaStream_t)stream);
+    h->status = st;
+    h->info.status = st;
+    h->info.device_bytes = h->arena.bytes;
+    h->info.analysis_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (st == SPTRSV_SUCCESS || st == SPTRSV_ERR_INVALID_MATRIX || st == SPTRSV_ERR_ZERO_PIVOT) {
+        *out = h;
+        return st;
+    }
+    h->arena.release_all();
+    delete h;
+    return st;
+}
+
+extern "C" sptrsv_status_t sptrsv_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs,
+                                        sptrsv_stream_t stream) {
+    if (!h || nrhs < 1) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) return SPTRSV_SUCCESS;
+    if (!b || !x) return SPTRSV_ERR_INVALID_VALUE;
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    return solve_impl(h, b, x, nrhs, (cudaStream_t)stream);
+}
+
+extern "C" sptrsv_status_t sptrsv_solve_host(sptrsv_handle_t h, const void *b_host, void *x_host,
+                                             int32_t nrhs, sptrsv_stream_t stream) {
+    if (!h || nrhs < 1) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) return SPTRSV_SUCCESS;
+    if (!b_host || !x_host) return SPTRSV_ERR_INVALID_VALUE;
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)h->n * (size_t)nrhs * h->esize;
+    if (h->stage_bytes < 2 * bytes) {
+        if (h->d_stage) {
+            SPTRSV_CUDA(cudaStreamSynchronize(s));
+            cudaFree(h->d_stage);
+            h->info.device_bytes -= (int64_t)h->stage_bytes;
+            h->d_stage = nullptr;
+            h->stage_bytes = 0;
+        }
+        SPTRSV_CUDA(cudaMalloc(&h->d_stage, 2 * bytes));
+        h->stage_bytes = 2 * bytes;
+        h->info.device_bytes += (int64_t)h->stage_bytes;
+    }
+    char *db = (char *)h->d_stage;
+    char *dx = db + bytes;
+    SPTRSV_CUDA(cudaMemcpyAsync(db, b_host, bytes, cudaMemcpyHostToDevice, s));
+    sptrsv_status_t st = solve_impl(h, db, dx, nrhs, s);
+    if (st != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemcpyAsync(x_host, dx, bytes, cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
+    if (!h) return SPTRSV_SUCCESS;
+    cudaSetDevice(h->device);
+    h->arena.release_all();
+    if (h->d_stage) cudaFree(h->d_stage);
+    delete h;
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK)
+        return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (algo == SPTRSV_ALGO_BLOCK && !h->block.built && h->n > 0) {
+        SPTRSV_CUDA(cudaSetDevice(h->device));
+        sptrsv_status_t st = block_build(h, nullptr);
+        if (st != SPTRSV_SUCCESS) return st;
+        h->info.nblocks = h->block.nblocks;
+        h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
+    }
+    h->algo = algo;
+    h->info.algo = algo;
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" sptrsv_status_t sptrsv_get_info(sptrsv_handle_t h, sptrsv_info_t *info) {
+    if (!h || !info) return SPTRSV_ERR_INVALID_VALUE;
+    *info = h->info;
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" sptrsv_status_t sptrsv_get_levels(sptrsv_handle_t h, int32_t *lev, int32_t *ilev, int32_t *jlev) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) {
+        if (ilev) ilev[0] = 0;
+        return SPTRSV_SUCCESS;
+    }
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    if (lev) SPTRSV_CUDA(cudaMemcpy(lev, h->d_lev, sizeof(int32_t) * (size_t)h->n, cudaMemcpyDeviceToHost));
+    if (ilev)
+        SPTRSV_CUDA(cudaMemcpy(ilev, h->d_ilev, sizeof(int32_t) * ((size_t)h->info.nlev + 1), cudaMemcpyDeviceToHost));
+    if (jlev) SPTRSV_CUDA(cudaMemcpy(jlev, h->d_jlev, sizeof(int32_t) * (size_t)h->n, cudaMemcpyDeviceToHost));
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" sptrsv_status_t sptrsv_get_dep_counts(sptrsv_handle_t h, int32_t *dp) {
+    if (!h || !dp) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) return SPTRSV_SUCCESS;
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    SPTRSV_CUDA(cudaMemcpy(dp, h->d_dp, sizeof(int32_t) * (size_t)h->n, cudaMemcpyDeviceToHost));
+    return SPTRSV_SUCCESS;
+}
+
+extern "C" const char *sptrsv_status_string(sptrsv_status_t s) {
+    switch (s) {
+        case SPTRSV_SUCCESS: return "SPTRSV_SUCCESS";
+        case SPTRSV_ERR_INVALID_VALUE: return "SPTRSV_ERR_INVALID_VALUE";
+        case SPTRSV_ERR_INVALID_MATRIX: return "SPTRSV_ERR_INVALID_MATRIX";
+        case SPTRSV_ERR_ZERO_PIVOT: return "SPTRSV_ERR_ZERO_PIVOT";
+        case SPTRSV_ERR_ALLOC: return "SPTRSV_ERR_ALLOC";
+        case SPTRSV_ERR_CUDA: return "SPTRSV_ERR_CUDA";
+        case SPTRSV_ERR_NOT_SUPPORTED: return "SPTRSV_ERR_NOT_SUPPORTED";
+        case SPTRSV_ERR_TIMEOUT: return "SPTRSV_ERR_TIMEOUT";
+    }
+    return "SPTRSV_UNKNOWN_STATUS";
+}
+
+extern "C" const char *sptrsv_last_cuda_error(void) { return sptrsv::g_last_cuda; }

@@ -1,0 +1,108 @@
+// internal.h -- the handle and host-side helpers of libsptrsv (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "sptrsv.h"
+#include "common.cuh"
+
+namespace sptrsv {
+
+// Records the last CUDA error message (thread-local) and maps it to a status.
+sptrsv_status_t cuda_fail(cudaError_t e, const char *where);
+#define SPTRSV_CUDA(call)                                                   \
+    do {                                                                    \
+        cudaError_t _e = (call);                                            \
+        if (_e != cudaSuccess) return ::sptrsv::cuda_fail(_e, #call);       \
+    } while (0)
+
+// Device allocation bookkeeping of one handle.
+struct DevArena {
+    std::vector<void *> ptrs;
+    int64_t bytes = 0;
+    sptrsv_status_t alloc(void **p, size_t nbytes);
+    template <typename T> sptrsv_status_t alloc_n(T **p, size_t n) {
+        return alloc(reinterpret_cast<void **>(p), n * sizeof(T));
+    }
+    void release_all();
+};
+
+// Block-schedule (SPTRSV_ALGO_BLOCK) device data; see block.cu.
+struct BlockPlan {
+    bool built = false;
+    int32_t nblocks = 0;
+    int32_t threads = 0;
+    int32_t smem_slots = 0;        // x slots per CTA in shared memory
+    int32_t nsteps = 0;            // total (block, local level, pass) steps
+    int32_t *d_block_row0 = nullptr;    // [nblocks+1] natural-order row ranges
+    int32_t *d_block_step0 = nullptr;   // [nblocks+1] step ranges
+    int2 *d_steps = nullptr;            // [nsteps] {first position, nrows | width<<16}
+    int64_t *d_step_eptr = nullptr;     // [nsteps] entry offsets
+    int32_t *d_bperm = nullptr;         // [n] position -> row (block-local level order)
+    void *d_binvd = nullptr;            // [n] reciprocal diagonal by position
+    int32_t *d_bcol = nullptr;          // entries: >= 0 global column, < 0 smem slot ~s
+    void *d_bval = nullptr;
+    int64_t nent = 0;
+    int32_t *d_started = nullptr;       // [nblocks] epoch at which block prefilled its rows
+    int32_t *d_wait_ptr = nullptr;      // [nblocks+1] producer-block lists
+    int32_t *d_wait_blk = nullptr;
+    unsigned *d_ticket = nullptr;       // [2]
+    int32_t grid = 0;
+};
+
+}  // namespace sptrsv
+
+struct sptrsv_handle_s {
+    int32_t n = 0;
+    int32_t uplo = 0, diag = 0, dtype = 0, algo = SPTRSV_ALGO_SELF;
+    sptrsv_status_t status = SPTRSV_SUCCESS;
+    sptrsv_info_t info{};
+    int device = 0;
+    int num_sms = 0;
+    size_t esize = 8;                        // sizeof value type
+
+    sptrsv::DevArena arena;
+    // analysis results
+    int32_t *d_dp = nullptr;                 // [n] dependency counts
+    int32_t *d_lev = nullptr;                // [n]
+    int32_t *d_ilev = nullptr;               // [nlev+1]
+    int32_t *d_jlev = nullptr;               // [n]
+    void *d_invd_row = nullptr;              // [n] 1/d(i) by row (dtype)
+    // level-ordered layout (SELF / LEVEL / MRHS)
+    int32_t nchunks = 0;
+    sptrsv::ChunkDesc *d_chunks = nullptr;   // [nchunks]
+    int32_t *d_lev_chunk = nullptr;          // [nlev+1]
+    int32_t *d_perm = nullptr;               // [n] solve position -> row
+    void *d_invd = nullptr;                  // [n] 1/d by solve position
+    int32_t *d_ecol = nullptr;
+    void *d_eval = nullptr;
+    int64_t nent = 0;
+    // synchronisation state
+    int32_t *d_flags = nullptr;              // [n] per-row ready flags (epoch tagged)
+    int32_t epoch = 0;
+    unsigned *d_ctr = nullptr;               // [0] ticket, [1] exit count (self / mrhs)
+    unsigned long long *d_bar = nullptr;     // level barrier counter (monotone)
+    unsigned long long bar_base = 0;
+    int32_t self_grid = 0, level_grid = 0, mrhs_grid = 0;
+    // in-place / host staging
+    void *d_stage = nullptr;
+    size_t stage_bytes = 0;
+    sptrsv::BlockPlan block;
+};
+
+namespace sptrsv {
+sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
+                             const void *vals, cudaStream_t s);
+sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);
+sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s);
+sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
+// device scans (analyze.cu)
+sptrsv_status_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
+sptrsv_status_t exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
+sptrsv_status_t radix_sort_pairs(const uint32_t *keys_in, const int32_t *vals_in, uint32_t *keys_out,
+                                 int32_t *vals_out, int64_t n, uint32_t max_key, DevArena &tmp,
+                                 cudaStream_t s);
+}  // namespace sptrsv

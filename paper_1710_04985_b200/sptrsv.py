@@ -1,0 +1,251 @@
+"""Thin ctypes binding of include/sptrsv.h -- argument marshalling only.
+
+Every step of the path runs in libsptrsv.so (hand-written sm_100a kernels).
+There is no fallback: if the library is missing or fails to load, importing
+this module raises.  torch supplies device memory and streams only.
+
+Low-level functions keep the C names (``sptrsv_analyze`` ... ``sptrsv_status_string``);
+``TriangularSolver`` wraps a handle for tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+LOWER, UPPER = 0, 1
+NON_UNIT, UNIT = 0, 1
+F64, F32 = 0, 1
+ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK = 0, 1, 2
+ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK}
+UPLO = {"lower": LOWER, "upper": UPPER}
+DIAG = {"non_unit": NON_UNIT, "unit": UNIT}
+
+STATUS_NAMES = {0: "SUCCESS", 1: "INVALID_VALUE", 2: "INVALID_MATRIX", 3: "ZERO_PIVOT", 4: "ALLOC",
+                5: "CUDA", 6: "NOT_SUPPORTED", 7: "TIMEOUT"}
+
+
+class sptrsv_info_t(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int32), ("nlev", ctypes.c_int32), ("max_level_width", ctypes.c_int32),
+        ("zero_pivot_row", ctypes.c_int32), ("bad_row", ctypes.c_int32),
+        ("uplo", ctypes.c_int32), ("diag", ctypes.c_int32), ("dtype", ctypes.c_int32),
+        ("algo", ctypes.c_int32), ("max_row_deps", ctypes.c_int32),
+        ("nnz_input", ctypes.c_int64), ("nnz_used", ctypes.c_int64), ("ignored_entries", ctypes.c_int64),
+        ("status", ctypes.c_int32), ("nblocks", ctypes.c_int32),
+        ("analysis_ms", ctypes.c_double), ("device_bytes", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsptrsv.so not built at {LIB_PATH}: run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32 = ctypes.c_void_p, ctypes.c_int32
+    lib.sptrsv_analyze.restype = ctypes.c_int
+    lib.sptrsv_analyze.argtypes = [i32, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp,
+                                   ctypes.POINTER(vp)]
+    lib.sptrsv_solve.restype = ctypes.c_int
+    lib.sptrsv_solve.argtypes = [vp, vp, vp, i32, vp]
+    lib.sptrsv_solve_host.restype = ctypes.c_int
+    lib.sptrsv_solve_host.argtypes = [vp, vp, vp, i32, vp]
+    lib.sptrsv_destroy.restype = ctypes.c_int
+    lib.sptrsv_destroy.argtypes = [vp]
+    lib.sptrsv_set_algo.restype = ctypes.c_int
+    lib.sptrsv_set_algo.argtypes = [vp, ctypes.c_int]
+    lib.sptrsv_get_info.restype = ctypes.c_int
+    lib.sptrsv_get_info.argtypes = [vp, ctypes.POINTER(sptrsv_info_t)]
+    lib.sptrsv_get_levels.restype = ctypes.c_int
+    lib.sptrsv_get_levels.argtypes = [vp, vp, vp, vp]
+    lib.sptrsv_get_dep_counts.restype = ctypes.c_int
+    lib.sptrsv_get_dep_counts.argtypes = [vp, vp]
+    lib.sptrsv_status_string.restype = ctypes.c_char_p
+    lib.sptrsv_status_string.argtypes = [ctypes.c_int]
+    lib.sptrsv_last_cuda_error.restype = ctypes.c_char_p
+    lib.sptrsv_last_cuda_error.argtypes = []
+    return lib
+
+
+_lib = _load()
+
+
+class SptrsvError(RuntimeError):
+    def __init__(self, status: int, where: str, info: dict | None = None):
+        name = STATUS_NAMES.get(status, str(status))
+        extra = ""
+        if status == 5:
+            extra = " (" + _lib.sptrsv_last_cuda_error().decode() + ")"
+        super().__init__(f"{where}: {name}{extra}")
+        self.status = status
+        self.name = name
+        self.info = info or {}
+
+
+# ----------------------------------------------------------- C-named calls
+def sptrsv_status_string(status: int) -> str:
+    return _lib.sptrsv_status_string(status).decode()
+
+
+def sptrsv_analyze(n, rowptr_ptr, colidx_ptr, vals_ptr, uplo, diag, dtype, stream_ptr):
+    """Returns (status, handle or None) exactly as the C call does."""
+    h = ctypes.c_void_p()
+    st = _lib.sptrsv_analyze(int(n), rowptr_ptr, colidx_ptr, vals_ptr, int(uplo), int(diag), int(dtype),
+                             stream_ptr, ctypes.byref(h))
+    return st, (h.value if h.value else None)
+
+
+def sptrsv_solve(handle, b_ptr, x_ptr, nrhs, stream_ptr) -> int:
+    return _lib.sptrsv_solve(handle, b_ptr, x_ptr, int(nrhs), stream_ptr)
+
+
+def sptrsv_solve_host(handle, b_ptr, x_ptr, nrhs, stream_ptr) -> int:
+    return _lib.sptrsv_solve_host(handle, b_ptr, x_ptr, int(nrhs), stream_ptr)
+
+
+def sptrsv_destroy(handle) -> int:
+    return _lib.sptrsv_destroy(handle)
+
+
+def sptrsv_set_algo(handle, algo) -> int:
+    return _lib.sptrsv_set_algo(handle, int(algo))
+
+
+def sptrsv_get_info(handle):
+    info = sptrsv_info_t()
+    st = _lib.sptrsv_get_info(handle, ctypes.byref(info))
+    return st, info
+
+
+def sptrsv_get_levels(handle, lev_ptr, ilev_ptr, jlev_ptr) -> int:
+    return _lib.sptrsv_get_levels(handle, lev_ptr, ilev_ptr, jlev_ptr)
+
+
+def sptrsv_get_dep_counts(handle, dp_ptr) -> int:
+    return _lib.sptrsv_get_dep_counts(handle, dp_ptr)
+
+
+# ------------------------------------------------------------- wrapper
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else None
+
+
+class TriangularSolver:
+    """Analyzed triangular factor on the current CUDA device.
+
+    rowptr/colidx: int32 CUDA tensors; vals: float64/float32 CUDA tensor (the
+    value dtype selects the solve precision).  The inputs may be freed after
+    construction (the handle copies what it needs).
+    """
+
+    def __init__(self, n, rowptr, colidx, vals, uplo="lower", diag="non_unit", algo="self", stream=None):
+        import torch
+        dtype = F64 if vals is None or vals.dtype == torch.float64 else F32
+        if vals is not None and vals.dtype not in (torch.float64, torch.float32):
+            raise TypeError("vals must be float64 or float32")
+        self.torch_dtype = torch.float64 if dtype == F64 else torch.float32
+        self.n = int(n)
+        for t in (rowptr, colidx):
+            if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+                raise TypeError("rowptr/colidx must be contiguous int32 CUDA tensors")
+        st, h = sptrsv_analyze(self.n, _dptr(rowptr), _dptr(colidx), _dptr(vals), UPLO[uplo], DIAG[diag],
+                               dtype, _stream_ptr(stream))
+        self.handle = h
+        if st != 0:
+            info = self.info() if h else {}
+            if h:
+                sptrsv_destroy(h)
+                self.handle = None
+            raise SptrsvError(st, "sptrsv_analyze", info)
+        if algo != "self":
+            self.set_algo(algo)
+
+    def set_algo(self, algo: str):
+        st = sptrsv_set_algo(self.handle, ALGOS[algo])
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_set_algo")
+
+    def info(self) -> dict:
+        st, info = sptrsv_get_info(self.handle)
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_get_info")
+        return info.as_dict()
+
+    def levels(self):
+        info = self.info()
+        lev = np.zeros(max(self.n, 1), dtype=np.int32)
+        ilev = np.zeros(info["nlev"] + 1, dtype=np.int32)
+        jlev = np.zeros(max(self.n, 1), dtype=np.int32)
+        st = sptrsv_get_levels(self.handle, lev.ctypes.data_as(ctypes.c_void_p),
+                               ilev.ctypes.data_as(ctypes.c_void_p), jlev.ctypes.data_as(ctypes.c_void_p))
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_get_levels")
+        return lev[:self.n], ilev, jlev[:self.n], info["nlev"]
+
+    def dep_counts(self):
+        dp = np.zeros(max(self.n, 1), dtype=np.int32)
+        st = sptrsv_get_dep_counts(self.handle, dp.ctypes.data_as(ctypes.c_void_p))
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_get_dep_counts")
+        return dp[:self.n]
+
+    def solve(self, b, x=None, stream=None):
+        """x = T^{-1} b for a CUDA tensor b of shape (n,) or (n, nrhs), row-major."""
+        import torch
+        if b.dtype != self.torch_dtype or not b.is_cuda or not b.is_contiguous():
+            raise TypeError(f"b must be a contiguous {self.torch_dtype} CUDA tensor")
+        nrhs = 1 if b.dim() == 1 else b.shape[1]
+        if x is None:
+            x = torch.empty_like(b)
+        st = sptrsv_solve(self.handle, _dptr(b), _dptr(x), nrhs, _stream_ptr(stream))
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_solve")
+        return x
+
+    def solve_host(self, b, x=None, stream=None):
+        """The same solve on HOST arrays (numpy or CPU tensors); copies are inside the call."""
+        nrhs = 1 if b.ndim == 1 else b.shape[1]
+        if x is None:
+            x = np.empty_like(b) if isinstance(b, np.ndarray) else b.new_empty(b.shape)
+        bp = b.ctypes.data_as(ctypes.c_void_p) if isinstance(b, np.ndarray) else ctypes.c_void_p(b.data_ptr())
+        xp = x.ctypes.data_as(ctypes.c_void_p) if isinstance(x, np.ndarray) else ctypes.c_void_p(x.data_ptr())
+        st = sptrsv_solve_host(self.handle, bp, xp, nrhs, _stream_ptr(stream))
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_solve_host")
+        return x
+
+    def close(self):
+        if getattr(self, "handle", None):
+            sptrsv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_csr(m, uplo="lower", diag="non_unit", dtype=None, algo="self", device="cuda"):
+    """Upload a host CSR (workloads.CSR-like: n, rowptr, colidx, vals) and analyze it."""
+    import torch
+    dt = torch.float64 if dtype in (None, np.float64, torch.float64) else torch.float32
+    rp = torch.from_numpy(np.ascontiguousarray(m.rowptr, dtype=np.int32)).to(device)
+    ci = torch.from_numpy(np.ascontiguousarray(m.colidx, dtype=np.int32)).to(device)
+    va = torch.from_numpy(np.ascontiguousarray(m.vals)).to(device=device, dtype=dt)
+    return TriangularSolver(m.n, rp, ci, va, uplo, diag, algo)

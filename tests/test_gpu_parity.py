@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Analysis outputs (dp, lev, nlev, ilev, jlev) must match bit for bit; solutions
+within the north-star tolerance: ||x - x_ref||_inf / ||x_ref||_inf <= 1e-10
+(fp64), 1e-4 (fp32); integer-exact systems bit for bit.  Inputs are seeded
+and synthetic (workloads/), at the five BASELINE.json configurations'
+full sizes plus small cases that span several chunks and ragged tails.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from workloads import CSR
+
+from test_oracle_levels import chain, random_triangular
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+TOL = {np.float64: 1e-10, np.float32: 1e-4}
+ALGOS = ["self", "level"]
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1710_04985_b200 import sptrsv
+    return sptrsv
+
+
+def relerr(x, ref):
+    x = np.asarray(x, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    den = np.abs(ref).max() if ref.size else 1.0
+    return float(np.abs(x - ref).max() / den) if ref.size else 0.0
+
+
+def gpu_solve(S, m, b, uplo="lower", diag="non_unit", dtype=np.float64, algo="self", solver=None):
+    solver = solver or S.from_csr(m, uplo, diag, dtype, algo)
+    bt = torch.from_numpy(np.ascontiguousarray(b, dtype=dtype)).cuda()
+    x = solver.solve(bt)
+    torch.cuda.synchronize()
+    return x.cpu().numpy(), solver
+
+
+def check_analysis(S, m, uplo, diag):
+    ref = oracle.analyze(m, uplo, diag)
+    assert ref["status"] == "SUCCESS"
+    sv = S.from_csr(m, uplo, diag)
+    lev, ilev, jlev, nlev = sv.levels()
+    info = sv.info()
+    assert nlev == ref["nlev"]
+    assert np.array_equal(sv.dep_counts(), ref["dp"])
+    assert np.array_equal(lev, ref["lev"])
+    assert np.array_equal(ilev, ref["ilev"])
+    assert np.array_equal(jlev, ref["jlev"])
+    assert info["nnz_used"] == ref["nnz_used"]
+    assert info["ignored_entries"] == ref["ignored"]
+    assert info["max_level_width"] == ref["max_level_width"]
+    assert info["max_row_deps"] == (int(ref["dp"].max()) if m.n else 0)
+    return sv
+
+
+# ------------------------------------------------------------ analysis
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_analysis_bit_exact_full_configs(S, cfg):
+    m, p = workloads.config(cfg)
+    check_analysis(S, m, p["uplo"], p["diag"])
+
+
+def test_analysis_bit_exact_cfg3_both_factors(S):
+    m, _ = workloads.config(3)
+    check_analysis(S, m, "lower", "unit")
+    check_analysis(S, m, "upper", "non_unit")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_analysis_random_small(S, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 3000))
+    uplo = ("lower", "upper")[seed % 2]
+    m = random_triangular_fast(n, float(rng.uniform(1, 40)), seed, uplo)
+    check_analysis(S, m, uplo, "non_unit")
+
+
+def random_triangular_fast(n, avg_deps, seed, uplo, other=0.5):
+    """Random triangle with a stored diagonal, some opposite-triangle entries,
+    and a few long rows (> 16 deps -> warp-per-row)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        lo, hi = (0, i) if uplo == "lower" else (i + 1, n)
+        span = hi - lo
+        k = min(span, int(rng.poisson(avg_deps)) if rng.random() > 0.02 else int(rng.integers(17, 200)))
+        deps = rng.choice(span, size=k, replace=False) + lo if k > 0 else np.zeros(0, dtype=np.int64)
+        olo, ohi = (i + 1, n) if uplo == "lower" else (0, i)
+        no = min(ohi - olo, int(rng.poisson(other)))
+        oth = rng.choice(ohi - olo, size=no, replace=False) + olo if no > 0 else np.zeros(0, dtype=np.int64)
+        rows.append(np.unique(np.concatenate([deps, oth, [i]]).astype(np.int64)))
+    rowptr = np.zeros(n + 1, dtype=np.int32)
+    rowptr[1:] = np.cumsum([len(r) for r in rows])
+    colidx = np.concatenate(rows).astype(np.int32) if n else np.zeros(0, dtype=np.int32)
+    vals = rng.uniform(-1, 1, size=colidx.size)
+    for i in range(n):
+        a, b = rowptr[i], rowptr[i + 1]
+        k = a + int(np.searchsorted(colidx[a:b], i))
+        vals[k] = (1.0 + np.abs(vals[a:b]).sum()) * (1 if rng.random() < 0.5 else -1)
+    return CSR(n, rowptr, colidx, vals)
+
+
+# ------------------------------------------------------------ solves
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_solve_full_configs(S, cfg, algo):
+    m, p = workloads.config(cfg)
+    b = workloads.rhs(m.n, 1, seed=p["seed"])[:, 0]
+    ref = oracle.solve(m, b, p["uplo"], p["diag"])
+    x, sv = gpu_solve(S, m, b, p["uplo"], p["diag"], algo=algo)
+    assert relerr(x, ref) <= TOL[np.float64]
+    # run-to-run bitwise reproducible
+    x2, _ = gpu_solve(S, m, b, solver=sv)
+    assert np.array_equal(x, x2)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_cfg3_pair_solve_full(S, algo):
+    m, p = workloads.config(3)
+    b = workloads.rhs(m.n, 1, seed=p["seed"])[:, 0]
+    ref = oracle.pair_solve(m, b)
+    lo = S.from_csr(m, "lower", "unit", algo=algo)
+    up = S.from_csr(m, "upper", "non_unit", algo=algo)
+    bt = torch.from_numpy(b).cuda()
+    y = up.solve(lo.solve(bt))
+    assert relerr(y.cpu().numpy(), ref) <= TOL[np.float64]
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("uplo,diag", [("lower", "non_unit"), ("upper", "non_unit"), ("lower", "unit"),
+                                       ("upper", "unit")])
+def test_solve_random_small(S, uplo, diag, dtype, algo):
+    for seed in range(4):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(1, 2500))
+        m = random_triangular_fast(n, float(rng.uniform(1, 20)), 10 * seed + 1, uplo)
+        if diag == "unit":
+            off = m.colidx != np.repeat(np.arange(n), np.diff(m.rowptr))
+            m.vals[off] *= 0.5 / max(1.0, np.diff(m.rowptr).max())
+        b = workloads.rhs(n, 1, seed=seed)[:, 0]
+        ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, diag, dtype=dtype)
+        x, _ = gpu_solve(S, m, b, uplo, diag, dtype, algo)
+        assert relerr(x, ref) <= TOL[dtype], (seed, n)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["cfg1", "7pt_d8", "7pt_upper_d8"])
+def test_integer_exact_bitwise(S, case, dtype, algo):
+    if case == "cfg1":
+        m, uplo = workloads.stencil((32, 32), 5, "lower"), "lower"
+    elif case == "7pt_d8":
+        m, uplo = workloads.stencil((40, 30, 20), 7, "lower", diag=8.0), "lower"
+    else:
+        m, uplo = workloads.stencil((40, 30, 20), 7, "upper", diag=8.0), "upper"
+    xt = workloads.integer_xtrue(m.n, 1, seed=101)[:, 0]
+    b = oracle.matvec(m, xt, uplo)
+    x, _ = gpu_solve(S, m, b, uplo, dtype=dtype, algo=algo)
+    assert np.array_equal(x.astype(np.float64), xt)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_backward_error_bound_gpu(S, algo):
+    m, p = workloads.config(2, scale=0.5)
+    b = workloads.rhs(m.n, 1, seed=9)[:, 0]
+    x, _ = gpu_solve(S, m, b, algo=algo)
+    k = 3
+    u = 2.0 ** -53
+    assert oracle.backward_error(m, b, x) <= (k + 2) * u / (1 - (k + 2) * u)
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_chain_progress(S, algo):
+    # P:315-316 worst case nlev = n: one long dependency chain
+    n = 100000
+    m = chain(n, sub=-0.5, d=1.0)
+    b = workloads.rhs(n, 1, seed=4)[:, 0]
+    x, _ = gpu_solve(S, m, b, algo=algo)
+    assert relerr(x, oracle.solve(m, b)) <= 1e-10
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_diagonal_and_tiny(S, algo):
+    for n in (1, 2, 31, 32, 33, 1000):
+        m = CSR(n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32),
+                np.linspace(1, 2, n))
+        b = workloads.rhs(n, 1, seed=n)[:, 0]
+        x, _ = gpu_solve(S, m, b, algo=algo)
+        assert relerr(x, b / m.vals) <= 1e-15
+
+
+def test_in_place_solve(S):
+    m, _ = workloads.config(2, scale=0.25)
+    b = workloads.rhs(m.n, 1, seed=3)[:, 0]
+    ref = oracle.solve(m, b)
+    for algo in ALGOS:
+        sv = S.from_csr(m, algo=algo)
+        bt = torch.from_numpy(b.copy()).cuda()
+        sv.solve(bt, x=bt)
+        assert relerr(bt.cpu().numpy(), ref) <= 1e-10
+
+
+def test_solve_host_matches(S):
+    m, _ = workloads.config(2, scale=0.25)
+    b = workloads.rhs(m.n, 2, seed=3)
+    sv = S.from_csr(m)
+    x = sv.solve_host(b)
+    assert relerr(x, oracle.solve(m, b)) <= 1e-10
+    x1 = sv.solve_host(np.ascontiguousarray(b[:, 0]))
+    assert relerr(x1, oracle.solve(m, b[:, 0])) <= 1e-10
+
+
+# ------------------------------------------------------------ multi-RHS
+@pytest.mark.parametrize("nrhs", [2, 3, 33, 64])
+def test_multi_rhs_small(S, nrhs):
+    m = random_triangular_fast(3000, 6.0, 5, "lower")
+    b = workloads.rhs(m.n, nrhs, seed=nrhs)
+    x, _ = gpu_solve(S, m, b)
+    assert relerr(x, oracle.solve(m, b)) <= 1e-10
+
+
+def test_cfg5_full_64_rhs_and_partition_bitwise(S):
+    # cfg5: 64 RHS on the 128^3 factor; column blocks (G = 2, 4, 8) must equal
+    # the G = 1 columns bit for bit, and match the oracle
+    m, _ = workloads.config(5)
+    b = workloads.rhs_columns(m.n, range(64))
+    sv = S.from_csr(m)
+    x_all = sv.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+    cols = [0, 17, 40, 63]
+    ref = oracle.solve(m, np.ascontiguousarray(b[:, cols]))
+    assert relerr(x_all[:, cols], ref) <= 1e-10
+    from paper_1710_04985_b200 import partition
+    for G in (2, 4, 8):
+        for r in range(G):
+            a, e = partition.block_range(64, G, r)
+            xb = sv.solve(torch.from_numpy(np.ascontiguousarray(b[:, a:e])).cuda()).cpu().numpy()
+            assert np.array_equal(xb, x_all[:, a:e])
+
+
+def test_multi_rhs_columns_equal_single_rhs_self(S):
+    # TPR rows use the same per-(row, column) arithmetic in k_self and k_mrhs
+    m, _ = workloads.config(2, scale=0.25)
+    b = workloads.rhs(m.n, 4, seed=8)
+    sv = S.from_csr(m)
+    xm = sv.solve(torch.from_numpy(b).cuda()).cpu().numpy()
+    for r in range(4):
+        xs = sv.solve(torch.from_numpy(np.ascontiguousarray(b[:, r])).cuda()).cpu().numpy()
+        assert np.array_equal(xs, xm[:, r])
+
+
+# ------------------------------------------------------------ status codes
+def _upload(m):
+    rp = torch.from_numpy(np.ascontiguousarray(m.rowptr, dtype=np.int32)).cuda()
+    ci = torch.from_numpy(np.ascontiguousarray(m.colidx, dtype=np.int32)).cuda()
+    va = torch.from_numpy(np.ascontiguousarray(m.vals, dtype=np.float64)).cuda()
+    return rp, ci, va
+
+
+def test_status_codes_match_oracle(S):
+    from test_oracle_solve import csr
+    cases = [
+        (csr(3, [[0], [1, 0], [1, 2]]), "lower", "non_unit"),
+        (csr(3, [[0], [0, 1], [1, 3]]), "lower", "non_unit"),
+        (csr(3, [[0], [0], [1, 2]]), "lower", "non_unit"),
+        (csr(3, [[0], [0], [1, 2]]), "lower", "unit"),
+        (csr(3, [[0], [0, 1], [1, 2]], vals=[1, 1, 1, 1, 0.0]), "lower", "non_unit"),
+        (csr(3, [[0], [0], [2, 1]]), "upper", "non_unit"),
+    ]
+    for m, uplo, diag in cases:
+        ref = oracle.select(m, uplo, diag)
+        rp, ci, va = _upload(m)
+        if ref["status"] == "SUCCESS":
+            S.TriangularSolver(m.n, rp, ci, va, uplo, diag).close()
+            continue
+        with pytest.raises(S.SptrsvError) as e:
+            S.TriangularSolver(m.n, rp, ci, va, uplo, diag)
+        assert e.value.name == ref["status"]
+        assert e.value.info["bad_row"] == ref["bad_row"]
+        assert e.value.info["zero_pivot_row"] == ref["zero_pivot_row"]
+    # bad rowptr[0]
+    m = csr(3, [[0], [0, 1], [1, 2]])
+    m.rowptr = m.rowptr.copy()
+    m.rowptr[0] = 1
+    rp, ci, va = _upload(m)
+    with pytest.raises(S.SptrsvError) as e:
+        S.TriangularSolver(3, rp, ci, va)
+    assert e.value.name == "INVALID_MATRIX" and e.value.info["bad_row"] == 0
+
+
+def test_invalid_value_and_empty(S):
+    m = CSR(0, np.zeros(1, dtype=np.int32), np.zeros(0, dtype=np.int32), np.zeros(0))
+    rp, ci, va = _upload(m)
+    sv = S.TriangularSolver(0, rp, ci, va)
+    assert sv.info()["nlev"] == 0
+    assert sv.solve(torch.zeros(0, dtype=torch.float64, device="cuda")).numel() == 0
+    m2, _ = workloads.config(1)
+    sv2 = S.from_csr(m2)
+    b = torch.zeros(m2.n, dtype=torch.float64, device="cuda")
+    assert S.sptrsv_solve(sv2.handle, S._dptr(b), S._dptr(b), 0, None) == 1   # nrhs < 1
+    assert S.sptrsv_set_algo(sv2.handle, 9) == 1

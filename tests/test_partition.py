@@ -1,0 +1,62 @@
+"""Batch partitioner (a10) -- host logic, plus a world_size-2 gloo run of the
+gather path (the same code the multi-GPU bench uses, over CPU tensors)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_1710_04985_b200 import partition
+
+
+@pytest.mark.parametrize("total,ws", [(64, 1), (64, 2), (64, 4), (64, 8), (10, 3), (3, 8), (0, 4)])
+def test_block_range_covers_exactly(total, ws):
+    ranges = partition.all_ranges(total, ws)
+    assert ranges[0][0] == 0 and ranges[-1][1] == total
+    for (a, b), (c, d) in zip(ranges, ranges[1:]):
+        assert b == c and a <= b
+    sizes = [b - a for a, b in ranges]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_block_range_rejects_bad_args():
+    with pytest.raises(ValueError):
+        partition.block_range(8, 0, 0)
+    with pytest.raises(ValueError):
+        partition.block_range(8, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, ws, port, total, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    a, b = partition.block_range(total, ws, rank)
+    n = 5
+    # each rank "solves" its columns: column r of the result is r + 100*i
+    local = torch.tensor([[float(r + 100 * i) for r in range(a, b)] for i in range(n)],
+                         dtype=torch.float64).reshape(n, b - a)
+    full = partition.gather_columns(local, total)
+    out[rank] = full.tolist()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [64, 7])
+def test_gather_columns_gloo_world2(total):
+    ws = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(ws, port, total, out), nprocs=ws, join=True)
+    expect = [[float(r + 100 * i) for r in range(total)] for i in range(5)]
+    for r in range(ws):
+        assert out[r] == expect
