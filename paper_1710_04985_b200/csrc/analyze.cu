@@ -366,10 +366,12 @@ __global__ void k_chunks_per_level(const int32_t *ilev, const int32_t *wcnt, int
 
 // one thread per level writes that level's chunk descriptors and entry counts
 __global__ void k_chunk_desc(const int32_t *ilev, const int32_t *wcnt, const int32_t *lev_chunk, int nlev,
-                             const int32_t *perm, const int32_t *dp, ChunkDesc *chunks, int64_t *ecount) {
+                             const int32_t *perm, const int32_t *dp, ChunkDesc *chunks, int64_t *ecount,
+                             int32_t *chunk_lev) {
     int l = blockIdx.x * blockDim.x + threadIdx.x;
     if (l >= nlev) return;
     int c = lev_chunk[l];
+    for (int cc = lev_chunk[l]; cc < lev_chunk[l + 1]; ++cc) chunk_lev[cc] = l;
     const int p0 = ilev[l], p1 = ilev[l + 1], w = wcnt[l];
     for (int p = p0; p < p0 + w; ++p, ++c) {
         int len = dp[perm[p]];
@@ -547,8 +549,12 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     if ((st = tmp.alloc_n(&ecount, (size_t)nchunks + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&eptr, (size_t)nchunks + 1)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(ecount, 0, sizeof(int64_t) * ((size_t)nchunks + 1), s));
+    if ((st = h->arena.alloc_n(&h->d_chunk_lev, (size_t)nchunks + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&h->d_done, (size_t)nlev + 1)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(h->d_done, 0, sizeof(unsigned) * ((size_t)nlev + 1), s));
+    h->self_epoch = 0;
     k_chunk_desc<<<(nlev + 127) / 128, 128, 0, s>>>(h->d_ilev, wcnt, h->d_lev_chunk, nlev, h->d_perm, h->d_dp,
-                                                     h->d_chunks, ecount);
+                                                     h->d_chunks, ecount, h->d_chunk_lev);
     SPTRSV_CUDA(cudaGetLastError());
     if ((st = exclusive_scan_i64(ecount, eptr, (int64_t)nchunks + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     int64_t nent = 0;

@@ -138,6 +138,7 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
     cudaSetDevice(h->device);
     h->arena.release_all();
     if (h->d_stage) cudaFree(h->d_stage);
+    if (h->d_scratch) cudaFree(h->d_scratch);
     delete h;
     return SPTRSV_SUCCESS;
 }

@@ -33,24 +33,23 @@ struct DevArena {
 // Block-schedule (SPTRSV_ALGO_BLOCK) device data; see block.cu.
 struct BlockPlan {
     bool built = false;
-    int32_t nblocks = 0;
-    int32_t threads = 0;
-    int32_t smem_slots = 0;        // x slots per CTA in shared memory
-    int32_t nsteps = 0;            // total (block, local level, pass) steps
-    int32_t *d_block_row0 = nullptr;    // [nblocks+1] natural-order row ranges
-    int32_t *d_block_step0 = nullptr;   // [nblocks+1] step ranges
-    int2 *d_steps = nullptr;            // [nsteps] {first position, nrows | width<<16}
-    int64_t *d_step_eptr = nullptr;     // [nsteps] entry offsets
-    int32_t *d_bperm = nullptr;         // [n] position -> row (block-local level order)
-    void *d_binvd = nullptr;            // [n] reciprocal diagonal by position
-    int32_t *d_bcol = nullptr;          // entries: >= 0 global column, < 0 smem slot ~s
-    void *d_bval = nullptr;
-    int64_t nent = 0;
-    int32_t *d_started = nullptr;       // [nblocks] epoch at which block prefilled its rows
-    int32_t *d_wait_ptr = nullptr;      // [nblocks+1] producer-block lists
-    int32_t *d_wait_blk = nullptr;
-    unsigned *d_ticket = nullptr;       // [2]
-    int32_t grid = 0;
+    int32_t nblocks = 0;      // K co-resident CTAs
+    int32_t nunits = 0;       // K x warps per CTA
+    int32_t W = 0;            // shared-memory x slots per warp (power of two)
+    int32_t nst = 0;          // TMA records in flight per warp
+    int32_t nsteps = 0;       // (unit, level) steps of <= 32 rows
+    int32_t maxw = 0, novf = 0, threads = 0, rec_max = 0, max_unit_rows = 0, rows_per_step = 32;
+    int32_t grid_nx = 0, grid_ny = 0, tiles_x = 0, tiles_y = 0;   // detected grid / tiles (0 = natural)
+    int64_t nent = 0;         // record bytes
+    size_t smem = 0;
+    void *kernel = nullptr;
+    void *kernel_trace = nullptr;
+    int32_t *d_unit_step0 = nullptr;  // [U+1]
+    int64_t *d_rec_off = nullptr;     // [nsteps+1] byte offsets of the step records
+    void *d_recs = nullptr;           // step records (see block.cu)
+    int32_t *d_ovf_ptr = nullptr;     // [n+1] by position
+    int32_t *d_ovf_col = nullptr;
+    void *d_ovf_val = nullptr;
 };
 
 }  // namespace sptrsv
@@ -75,6 +74,9 @@ struct sptrsv_handle_s {
     int32_t nchunks = 0;
     sptrsv::ChunkDesc *d_chunks = nullptr;   // [nchunks]
     int32_t *d_lev_chunk = nullptr;          // [nlev+1]
+    int32_t *d_chunk_lev = nullptr;          // [nchunks] level of each chunk
+    unsigned *d_done = nullptr;              // [nlev] per-level completed-chunk counters (SELF hint)
+    unsigned self_epoch = 0;                 // SELF solves so far (done[l] == self_epoch * chunks(l))
     int32_t *d_perm = nullptr;               // [n] solve position -> row
     void *d_invd = nullptr;                  // [n] 1/d by solve position
     int32_t *d_ecol = nullptr;
@@ -90,6 +92,8 @@ struct sptrsv_handle_s {
     // in-place / host staging
     void *d_stage = nullptr;
     size_t stage_bytes = 0;
+    void *d_scratch = nullptr;               // copy of b for in-place value-as-flag solves
+    size_t scratch_bytes = 0;
     sptrsv::BlockPlan block;
 };
 

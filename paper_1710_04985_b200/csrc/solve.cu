@@ -1,9 +1,13 @@
 // solve.cu -- the solve phase over the level-ordered layout built by analyze.cu.
 //
 //   k_self   a6: self-scheduled solve (Alg. 3 SLFR; kernel P:577-619),
-//            re-expressed with PULL-style per-row ready flags: a row waits
-//            until flag[j] == epoch for each dependency j, computes, stores
-//            x(i), then publishes flag[i] = epoch with release semantics.
+//            re-expressed with PULL-style per-row ready flags.  The flag of row
+//            j is its value x(j) itself: x is prefilled with a NaN-payload
+//            sentinel (k_prefill) and a row spins on relaxed loads of its
+//            dependencies until none is the sentinel, then stores x(i) with a
+//            relaxed store.  64-bit aligned accesses are single-copy atomic,
+//            so no fence is needed (the paper's __threadfence, P:603, P:616-619,
+//            becomes unnecessary) -- one L2 round trip per handoff.
 //            Warps claim 32-row chunks by an atomic ticket in jlev order (the
 //            paper's warp-unknown mapping), so a wait only ever
 //            targets rows claimed earlier by running warps: deadlock-free for
@@ -51,12 +55,15 @@ __device__ __forceinline__ void wait_flags(const int *flags, const int (&cols)[N
 
 // ---------------------------------------------------------------- TPR row
 // One chunk of up to 32 rows, thread per row.  Entry k of lane r at
-// eptr + k*32 + r.  Returns with x(row) stored (not yet published).
+// eptr + k*32 + r.  WAIT: dependencies are polled as VALUES (value-as-flag,
+// x prefilled with Sentinel<T>): every pending value is re-loaded with a
+// relaxed (L2-coherent) load until it is no longer the sentinel -- one L2
+// round trip per handoff and no fences (B200 measurement: a fence after
+// stores costs ~580 ns, the relaxed handoff ~220 ns; profiles/).
 template <typename T, bool UNIT, bool WAIT>
 __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                           const T *__restrict__ invd, const int32_t *__restrict__ ecol,
-                                          const T *__restrict__ eval, const T *b, T *x, const int *flags,
-                                          int epoch, int &row_out, bool &act_out) {
+                                          const T *__restrict__ eval, const T *b, T *x) {
     const int nr = chunk_nrows(cd.meta), width = chunk_width(cd.meta);
     const bool act = lane < nr;
     int row = 0;
@@ -68,6 +75,7 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
     }
     int cols[kTprMax];
     T vals[kTprMax];
+    T xv[kTprMax];
     const int32_t *ec = ecol + cd.eptr + lane;
     const T *ev = eval + cd.eptr + lane;
 #pragma unroll
@@ -80,54 +88,74 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
         }
     }
     if (WAIT) {
-        wait_flags<kTprMax>(flags, cols, width, epoch);
-        fence_acq_rel_gpu();
+#pragma unroll
+        for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_relaxed_val(x + cols[k]) : T(0);
+        bool pend = false;
+#pragma unroll
+        for (int k = 0; k < kTprMax; ++k) pend |= (cols[k] >= 0) && Sentinel<T>::is(xv[k]);
+        while (pend) {
+            pend = false;
+            __nanosleep(20);
+#pragma unroll
+            for (int k = 0; k < kTprMax; ++k) {
+                if (cols[k] >= 0 && Sentinel<T>::is(xv[k])) {
+                    xv[k] = ld_relaxed_val(x + cols[k]);
+                    pend |= Sentinel<T>::is(xv[k]);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_cg(x + cols[k]) : T(0);
     }
 #pragma unroll
     for (int k = 0; k < kTprMax; ++k) {
-        if (k < width && cols[k] >= 0) s = fnma(vals[k], ld_cg(x + cols[k]), s);
+        if (cols[k] >= 0) s = fnma(vals[k], xv[k], s);
     }
-    if (act) x[row] = finish<T, UNIT>(s, di);
-    row_out = row;
-    act_out = act;
+    if (act) {
+        const T r = finish<T, UNIT>(s, di);
+        if (WAIT) st_relaxed_val(x + row, Sentinel<T>::scrub(r));
+        else x[row] = r;
+    }
 }
 
 // ---------------------------------------------------------------- WPR row
 template <typename T, bool UNIT, bool WAIT>
 __device__ __forceinline__ void wpr_row(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                         const T *__restrict__ invd, const int32_t *__restrict__ ecol,
-                                        const T *__restrict__ eval, const T *b, T *x, const int *flags,
-                                        int epoch, int &row_out) {
+                                        const T *__restrict__ eval, const T *b, T *x) {
     const int width = chunk_width(cd.meta);
     const int row = perm[cd.pos];
     const int32_t *ec = ecol + cd.eptr;
     const T *ev = eval + cd.eptr;
-    if (WAIT) {
-        for (int k = lane; k < width; k += 32) {
-            const int c = ec[k];
-            int spins = 0;
-            while (ld_relaxed(&flags[c]) != epoch) {
-                if (++spins > 8) __nanosleep(32);
-            }
-        }
-        __syncwarp();
-        fence_acq_rel_gpu();
-    }
     T acc = T(0);
-    for (int k = lane; k < width; k += 32) acc = __fma_rn(ld_stream(ev + k), ld_cg(x + ec[k]), acc);
+    for (int k = lane; k < width; k += 32) {
+        const int c = ec[k];
+        T v;
+        if (WAIT) {
+            v = ld_relaxed_val(x + c);
+            while (Sentinel<T>::is(v)) v = ld_relaxed_val(x + c);
+        } else {
+            v = ld_cg(x + c);
+        }
+        acc = __fma_rn(ld_stream(ev + k), v, acc);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[row] = finish<T, UNIT>(ld_cg(b + row) - acc, invd[cd.pos]);
-    row_out = row;
+    if (lane == 0) {
+        const T r = finish<T, UNIT>(ld_cg(b + row) - acc, invd[cd.pos]);
+        if (WAIT) st_relaxed_val(x + row, Sentinel<T>::scrub(r));
+        else x[row] = r;
+    }
 }
 
 // ---------------------------------------------------------------- SELF
+// x must hold Sentinel<T> in every row on entry (k_prefill).
 template <typename T, bool UNIT>
 __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__ chunks, int nchunks,
                                                    const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                    const int32_t *__restrict__ ecol, const T *__restrict__ eval,
-                                                   const T *b, T *x, int *flags, int epoch, unsigned *ctr,
-                                                   unsigned nwarps_total) {
+                                                   const T *b, T *x, unsigned *ctr, unsigned nwarps_total) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned t = 0;
@@ -135,16 +163,10 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
         t = __shfl_sync(0xffffffffu, t, 0);
         if ((int)t >= nchunks) break;
         const ChunkDesc cd = chunks[t];
-        if (!chunk_wpr(cd.meta)) {
-            int row;
-            bool act;
-            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, flags, epoch, row, act);
-            if (act) st_release(&flags[row], epoch);
-        } else {
-            int row;
-            wpr_row<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, flags, epoch, row);
-            if (lane == 0) st_release(&flags[row], epoch);
-        }
+        if (!chunk_wpr(cd.meta))
+            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x);
+        else
+            wpr_row<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x);
     }
     // the last warp out resets the ticket for the next solve on this stream
     if (lane == 0) {
@@ -154,6 +176,13 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
             ctr[1] = 0;
         }
     }
+}
+
+template <typename T>
+__global__ void k_prefill(T *x, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (; i < n; i += stride) x[i] = Sentinel<T>::value();
 }
 
 // ---------------------------------------------------------------- LEVEL
@@ -183,12 +212,10 @@ __global__ void __launch_bounds__(kThreads) k_level(const ChunkDesc *__restrict_
         const int c0 = lev_chunk[l], c1 = lev_chunk[l + 1];
         for (int c = c0 + gw; c < c1; c += nw) {
             const ChunkDesc cd = chunks[c];
-            int row;
-            bool act;
             if (!chunk_wpr(cd.meta))
-                tpr_chunk<T, UNIT, false>(cd, lane, perm, invd, ecol, eval, b, x, nullptr, 0, row, act);
+                tpr_chunk<T, UNIT, false>(cd, lane, perm, invd, ecol, eval, b, x);
             else
-                wpr_row<T, UNIT, false>(cd, lane, perm, invd, ecol, eval, b, x, nullptr, 0, row);
+                wpr_row<T, UNIT, false>(cd, lane, perm, invd, ecol, eval, b, x);
         }
         if (l + 1 < nlev) grid_barrier(bar, bar_base + (unsigned long long)(l + 1) * gridDim.x);
     }
@@ -285,6 +312,19 @@ __global__ void __launch_bounds__(kThreads) k_mrhs(const ChunkDesc *__restrict__
     }
 }
 
+sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes) {
+    if (h->scratch_bytes >= bytes) return SPTRSV_SUCCESS;
+    if (h->d_scratch) {
+        SPTRSV_CUDA(cudaDeviceSynchronize());
+        cudaFree(h->d_scratch);
+        h->d_scratch = nullptr;
+        h->scratch_bytes = 0;
+    }
+    SPTRSV_CUDA(cudaMalloc(&h->d_scratch, bytes));
+    h->scratch_bytes = bytes;
+    return SPTRSV_SUCCESS;
+}
+
 template <typename K>
 int resident_grid(K kernel, int num_sms) {
     int per_sm = 0;
@@ -317,9 +357,16 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
     if (nrhs == 1) {
         if (h->self_grid == 0) h->self_grid = resident_grid(k_self<T, UNIT>, h->num_sms);
         const int grid = h->self_grid;
+        if ((const void *)b == (const void *)x) {   // in place: keep b aside, x becomes the flag array
+            sptrsv_status_t st = ensure_scratch(h, (size_t)h->n * sizeof(T));
+            if (st != SPTRSV_SUCCESS) return st;
+            SPTRSV_CUDA(cudaMemcpyAsync(h->d_scratch, b, (size_t)h->n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+            b = (const T *)h->d_scratch;
+        }
+        k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n);
         k_self<T, UNIT><<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
-                                                  h->d_ecol, (const T *)h->d_eval, b, x, h->d_flags, h->epoch,
-                                                  h->d_ctr, (unsigned)(grid * (kThreads / 32)));
+                                                  h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
+                                                  (unsigned)(grid * (kThreads / 32)));
     } else {
         if (h->mrhs_grid == 0) h->mrhs_grid = resident_grid(k_mrhs<T, UNIT>, h->num_sms);
         const int grid = h->mrhs_grid;

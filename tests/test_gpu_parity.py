@@ -20,7 +20,7 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
 TOL = {np.float64: 1e-10, np.float32: 1e-4}
-ALGOS = ["self", "level"]
+ALGOS = ["self", "level", "block"]
 
 
 @pytest.fixture(scope="module")
@@ -36,11 +36,18 @@ def relerr(x, ref):
     return float(np.abs(x - ref).max() / den) if ref.size else 0.0
 
 
+def watchdog_clear(S):
+    """BLOCK's spin watchdog (debug hook): 1 means a wait gave up -- a scheduling bug."""
+    import ctypes
+    return ctypes.CDLL(S.LIB_PATH).sptrsv_dbg_watchdog() == 0
+
+
 def gpu_solve(S, m, b, uplo="lower", diag="non_unit", dtype=np.float64, algo="self", solver=None):
     solver = solver or S.from_csr(m, uplo, diag, dtype, algo)
     bt = torch.from_numpy(np.ascontiguousarray(b, dtype=dtype)).cuda()
     x = solver.solve(bt)
     torch.cuda.synchronize()
+    assert watchdog_clear(S)
     return x.cpu().numpy(), solver
 
 

@@ -112,7 +112,7 @@ int main() {
     CK(cudaGetDeviceProperties(&prop, 0));
     printf("{\"device\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"results\": {\n", prop.name, prop.multiProcessorCount, prop.l2CacheSize);
     int *flag; unsigned long long *out; unsigned *sms; int *sink; double *dsink;
-    CK(cudaMalloc(&flag, 1 << 20)); CK(cudaMalloc(&out, 4096)); CK(cudaMalloc(&sms, 64)); CK(cudaMalloc(&sink, 64)); CK(cudaMalloc(&dsink, 8 * 4096));
+    CK(cudaMalloc(&flag, 64 << 20)); CK(cudaMalloc(&out, 4096)); CK(cudaMalloc(&sms, 64)); CK(cudaMalloc(&sink, 64)); CK(cudaMalloc(&dsink, 8 * 4096));
     unsigned long long h[148];
     unsigned hs[2];
     const int iters = 20000;
