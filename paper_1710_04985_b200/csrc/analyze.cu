@@ -581,8 +581,9 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     SPTRSV_CUDA(cudaMemsetAsync(h->d_flags, 0, sizeof(int32_t) * (size_t)n, s));
     if ((st = h->arena.alloc_n(&h->d_ctr, 4)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(h->d_ctr, 0, sizeof(unsigned) * 4, s));
-    if ((st = h->arena.alloc_n(&h->d_bar, 1)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned long long), s));
+    // per-CTA arrival slots of the level-scheduled grid barrier (<= 64 CTAs per SM)
+    if ((st = h->arena.alloc_n(&h->d_bar, (size_t)h->num_sms * 64)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(h->d_bar, 0, sizeof(unsigned long long) * (size_t)h->num_sms * 64, s));
     h->epoch = 0;
     h->bar_base = 0;
 

@@ -82,6 +82,11 @@ struct sptrsv_handle_s {
     int32_t *d_ecol = nullptr;
     void *d_eval = nullptr;
     int64_t nent = 0;
+    // multi-RHS per-position CSR (built on the first nrhs > 1 solve)
+    bool mr_built = false;
+    int32_t *d_mr_ptr = nullptr;
+    int32_t *d_mr_col = nullptr;
+    void *d_mr_val = nullptr;
     // synchronisation state
     int32_t *d_flags = nullptr;              // [n] per-row ready flags (epoch tagged)
     int32_t epoch = 0;

@@ -186,11 +186,13 @@ __global__ void k_prefill(T *x, int64_t n) {
 }
 
 // ---------------------------------------------------------------- LEVEL
+// Grid barrier over the co-resident grid (one CTA per SM): arrival is a
+// release reduction on one monotone counter (no reset between solves), the
+// wait is one thread polling it with relaxed loads, then an acquire fence.
 __device__ __forceinline__ void grid_barrier(unsigned long long *bar, unsigned long long target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        fence_acq_rel_gpu();
-        atomicAdd(bar, 1ull);
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
         while (ld_relaxed_u64(bar) < target) {
         }
         fence_acq_rel_gpu();
@@ -198,8 +200,10 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *bar, unsigned l
     __syncthreads();
 }
 
+constexpr int kLevelThreads = 1024;
+
 template <typename T, bool UNIT>
-__global__ void __launch_bounds__(kThreads) k_level(const ChunkDesc *__restrict__ chunks,
+__global__ void __launch_bounds__(kLevelThreads, 1) k_level(const ChunkDesc *__restrict__ chunks,
                                                     const int32_t *__restrict__ lev_chunk, int nlev,
                                                     const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                     const int32_t *__restrict__ ecol, const T *__restrict__ eval,
@@ -222,85 +226,138 @@ __global__ void __launch_bounds__(kThreads) k_level(const ChunkDesc *__restrict_
 }
 
 // ---------------------------------------------------------------- MRHS
-// Warp per chunk; lane r polls the flags of chunk row r, then the warp walks
-// the rows with lanes over RHS columns.  Per (row, column) the arithmetic is
-// the TPR sequence, so each column equals the nrhs == 1 TPR result bitwise
-// and does not depend on nrhs (SURVEY §8e partition invariant).
-template <typename T, bool UNIT>
-__global__ void __launch_bounds__(kThreads) k_mrhs(const ChunkDesc *__restrict__ chunks, int nchunks,
-                                                   const int32_t *__restrict__ perm, const T *__restrict__ invd,
-                                                   const int32_t *__restrict__ ecol, const T *__restrict__ eval,
-                                                   const T *b, T *x, int nrhs, int *flags, int epoch,
-                                                   unsigned *ctr, unsigned nwarps_total) {
+// Multiple right-hand sides (a8).  Warp per ROW, lanes over the RHS columns
+// (CPL columns per lane), rows claimed by ticket in the solve order (levels
+// ascending), G rows per claim so that the b rows and entries of the next
+// rows are in flight while the first one waits on its dependencies.  One
+// ready flag per row (epoch-tagged): polled with acquire loads by the lanes
+// holding the dependencies, published with a release store after the row's
+// x values.  Per (row, column) the arithmetic is the TPR sequence, so each
+// column equals the nrhs == 1 TPR result bitwise and does not depend on nrhs
+// (SURVEY §8e partition invariant).  Entries come from a per-position CSR
+// (mr_*), built on the first multi-RHS solve.
+constexpr int kMrG = 4;
+
+template <typename T, bool UNIT, int CPL>
+__global__ void __launch_bounds__(kThreads) k_mrhs(int n, const int32_t *__restrict__ perm, const int32_t *__restrict__ lev,
+                                                   const T *__restrict__ invd,
+                                                   const int32_t *__restrict__ mr_ptr,
+                                                   const int32_t *__restrict__ mr_col, const T *__restrict__ mr_val,
+                                                   const T *b, T *x, int nrhs, int *flags, int epoch, unsigned *ctr,
+                                                   unsigned nwarps_total) {
     const int lane = threadIdx.x & 31;
     for (;;) {
         unsigned t = 0;
-        if (lane == 0) t = atomicAdd(&ctr[0], 1u);
+        if (lane == 0) t = atomicAdd(&ctr[0], (unsigned)kMrG);
         t = __shfl_sync(0xffffffffu, t, 0);
-        if ((int)t >= nchunks) break;
-        const ChunkDesc cd = chunks[t];
-        const int width = chunk_width(cd.meta);
-        if (!chunk_wpr(cd.meta)) {
-            const int nr = chunk_nrows(cd.meta);
-            const bool act = lane < nr;
-            int myrow = act ? perm[cd.pos + lane] : 0;
-            T mydi = act ? invd[cd.pos + lane] : T(0);
-            int cols[kTprMax];
-            T vals[kTprMax];
+        if ((int)t >= n) break;
+        int row[kMrG], e0[kMrG], deg[kMrG], col[kMrG];
+        T di[kMrG], val[kMrG];
+        T bv[kMrG][CPL];
+        // independent loads of all G rows first
 #pragma unroll
-            for (int k = 0; k < kTprMax; ++k) {
-                cols[k] = -1;
-                vals[k] = T(0);
-                if (k < width) {
-                    cols[k] = ld_stream(ecol + cd.eptr + k * 32 + lane);
-                    vals[k] = ld_stream(eval + cd.eptr + k * 32 + lane);
+        for (int g = 0; g < kMrG; ++g) {
+            const int p = (int)t + g;
+            row[g] = -1;
+            deg[g] = 0;
+            if (p < n) {
+                row[g] = perm[p];
+                di[g] = invd[p];
+                e0[g] = mr_ptr[p];
+                deg[g] = mr_ptr[p + 1] - e0[g];
+                col[g] = lane < deg[g] ? mr_col[e0[g] + lane] : -1;
+                val[g] = lane < deg[g] ? mr_val[e0[g] + lane] : T(0);
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const int c = lane + 32 * j;
+                    if (c < nrhs) bv[g][j] = ld_cg(b + (int64_t)row[g] * nrhs + c);
                 }
             }
-            wait_flags<kTprMax>(flags, cols, width, epoch);
-            fence_acq_rel_gpu();
-            __syncwarp();
-            for (int r = 0; r < nr; ++r) {
-                const int row = __shfl_sync(0xffffffffu, myrow, r);
-                const T di = __shfl_sync(0xffffffffu, mydi, r);
-                int rc[kTprMax];
-                T rv[kTprMax];
+        }
+        // concurrent path: all G rows valid, in one level, <= 8 dependencies each
+        // (rows of one level are independent): lane g*8+k polls dependency k of row g
+        bool conc = row[kMrG - 1] >= 0;
+        int lv = conc ? lev[row[0]] : 0;
 #pragma unroll
-                for (int k = 0; k < kTprMax; ++k) {
-                    rc[k] = __shfl_sync(0xffffffffu, cols[k], r);
-                    rv[k] = __shfl_sync(0xffffffffu, vals[k], r);
-                }
-                for (int c = lane; c < nrhs; c += 32) {
-                    T s = ld_cg(b + (int64_t)row * nrhs + c);
+        for (int g = 1; g < kMrG; ++g) conc = conc && lev[row[g]] == lv;
 #pragma unroll
-                    for (int k = 0; k < kTprMax; ++k) {
-                        if (k < width && rc[k] >= 0) s = fnma(rv[k], ld_cg(x + (int64_t)rc[k] * nrhs + c), s);
-                    }
-                    x[(int64_t)row * nrhs + c] = finish<T, UNIT>(s, di);
-                }
-            }
-            __syncwarp();
-            if (act) st_release(&flags[myrow], epoch);
-        } else {
-            const int row = perm[cd.pos];
-            const int32_t *ec = ecol + cd.eptr;
-            const T *ev = eval + cd.eptr;
-            for (int k = lane; k < width; k += 32) {
-                const int c = ec[k];
+        for (int g = 0; g < kMrG; ++g) conc = conc && deg[g] <= 8;
+        if (conc) {
+            const int gq = lane >> 3, kq = lane & 7;
+            int cq = -1;
+#pragma unroll
+            for (int g = 0; g < kMrG; ++g)
+                if (g == gq && kq < deg[g]) cq = mr_col[e0[g] + kq];
+            if (cq >= 0) {
                 int spins = 0;
-                while (ld_relaxed(&flags[c]) != epoch) {
-                    if (++spins > 8) __nanosleep(32);
+                while (ld_acquire(&flags[cq]) != epoch) {
+                    if (++spins > 4) __nanosleep(32);
                 }
             }
-            fence_acq_rel_gpu();
             __syncwarp();
-            const T di = invd[cd.pos];
-            for (int c = lane; c < nrhs; c += 32) {
-                T s = ld_cg(b + (int64_t)row * nrhs + c);
-                for (int k = 0; k < width; ++k) s = fnma(ev[k], ld_cg(x + (int64_t)ec[k] * nrhs + c), s);
-                x[(int64_t)row * nrhs + c] = finish<T, UNIT>(s, di);
+            T acc[kMrG][CPL];
+#pragma unroll
+            for (int g = 0; g < kMrG; ++g)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) acc[g][j] = bv[g][j];
+#pragma unroll
+            for (int g = 0; g < kMrG; ++g) {
+                for (int k = 0; k < deg[g]; ++k) {
+                    const int ck = __shfl_sync(0xffffffffu, col[g], k);
+                    const T vk = __shfl_sync(0xffffffffu, val[g], k);
+#pragma unroll
+                    for (int j = 0; j < CPL; ++j) {
+                        const int c = lane + 32 * j;
+                        if (c < nrhs) acc[g][j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[g][j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < kMrG; ++g)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const int c = lane + 32 * j;
+                    if (c < nrhs) x[(int64_t)row[g] * nrhs + c] = finish<T, UNIT>(acc[g][j], di[g]);
+                }
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < kMrG; ++g)
+                if (lane == g) st_release(&flags[row[g]], epoch);
+            continue;
+        }
+#pragma unroll
+        for (int g = 0; g < kMrG; ++g) {
+            if (row[g] < 0) break;
+            // wait for the dependencies (lane k polls dependency k)
+            for (int kb = 0; kb < deg[g]; kb += 32) {
+                const int c = (kb == 0) ? col[g] : (kb + lane < deg[g] ? mr_col[e0[g] + kb + lane] : -1);
+                if (c >= 0) {
+                    int spins = 0;
+                    while (ld_acquire(&flags[c]) != epoch) {
+                        if (++spins > 4) __nanosleep(32);
+                    }
+                }
             }
             __syncwarp();
-            if (lane == 0) st_release(&flags[row], epoch);
+            T acc[CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) acc[j] = bv[g][j];
+            for (int k = 0; k < deg[g]; ++k) {
+                const int ck = k < 32 ? __shfl_sync(0xffffffffu, col[g], k) : mr_col[e0[g] + k];
+                const T vk = k < 32 ? __shfl_sync(0xffffffffu, val[g], k) : mr_val[e0[g] + k];
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const int c = lane + 32 * j;
+                    if (c < nrhs) acc[j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+                const int c = lane + 32 * j;
+                if (c < nrhs) x[(int64_t)row[g] * nrhs + c] = finish<T, UNIT>(acc[j], di[g]);
+            }
+            __syncwarp();
+            if (lane == 0) st_release(&flags[row[g]], epoch);
         }
     }
     if (lane == 0) {
@@ -308,6 +365,136 @@ __global__ void __launch_bounds__(kThreads) k_mrhs(const ChunkDesc *__restrict__
         if (e == nwarps_total - 1) {
             ctr[0] = 0;
             ctr[1] = 0;
+        }
+    }
+}
+
+// Level-scheduled multiple right-hand sides (Alg. 1 LEVR over nrhs columns):
+// warp per row of the current level (grid-stride over the level's positions,
+// lanes over columns), then a grid barrier.  No flags: the barrier orders
+// the levels.  The b rows of the next level are prefetched into L2 before
+// the barrier.
+template <typename T, int CPL>
+struct MrRow {
+    int row, e0, deg, col;
+    T di, val;
+    T bv[CPL];
+};
+
+template <typename T, int CPL>
+__device__ __forceinline__ void mr_load(MrRow<T, CPL> &R, int p, int lane, const int32_t *__restrict__ perm,
+                                        const T *__restrict__ invd, const int32_t *__restrict__ mr_ptr,
+                                        const int32_t *__restrict__ mr_col, const T *__restrict__ mr_val, const T *b,
+                                        int nrhs) {
+    R.row = perm[p];
+    R.di = invd[p];
+    R.e0 = mr_ptr[p];
+    R.deg = mr_ptr[p + 1] - R.e0;
+    R.col = lane < R.deg ? mr_col[R.e0 + lane] : 0;
+    R.val = lane < R.deg ? mr_val[R.e0 + lane] : T(0);
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c < nrhs) R.bv[j] = ld_cg(b + (int64_t)R.row * nrhs + c);
+    }
+}
+
+template <typename T, bool UNIT, int CPL>
+__device__ __forceinline__ void mr_solve(const MrRow<T, CPL> &R, int lane, const int32_t *__restrict__ mr_col,
+                                         const T *__restrict__ mr_val, T *x, int nrhs) {
+    T acc[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) acc[j] = R.bv[j];
+    for (int k = 0; k < R.deg; ++k) {
+        const int ck = k < 32 ? __shfl_sync(0xffffffffu, R.col, k) : mr_col[R.e0 + k];
+        const T vk = k < 32 ? __shfl_sync(0xffffffffu, R.val, k) : mr_val[R.e0 + k];
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const int c = lane + 32 * j;
+            if (c < nrhs) acc[j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[j]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
+        if (c < nrhs) x[(int64_t)R.row * nrhs + c] = finish<T, UNIT>(acc[j], R.di);
+    }
+}
+
+// Level-scheduled multiple right-hand sides (Alg. 1 LEVR over nrhs columns):
+// warp per row of the current level (grid-stride over the level's positions,
+// lanes over columns), then a grid barrier.  No flags: the barrier orders the
+// levels.  Each warp loads the metadata and b of its FIRST row of the next
+// level before the barrier, so after it only the x loads of the dependencies
+// remain on the critical path.
+template <typename T, bool UNIT, int CPL>
+__global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *__restrict__ ilev, int nlev,
+                                                         const int32_t *__restrict__ perm, const T *__restrict__ invd,
+                                                         const int32_t *__restrict__ mr_ptr,
+                                                         const int32_t *__restrict__ mr_col,
+                                                         const T *__restrict__ mr_val, const T *b, T *x, int nrhs,
+                                                         unsigned long long *bar, unsigned long long bar_base) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    MrRow<T, CPL> pre;
+    int have = 0;
+    if (nlev > 0 && ilev[0] + gw < ilev[1]) {
+        mr_load(pre, ilev[0] + gw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+        have = 1;
+    }
+    for (int l = 0; l < nlev; ++l) {
+        const int p0 = ilev[l], p1 = ilev[l + 1];
+        if (have) mr_solve<T, UNIT, CPL>(pre, lane, mr_col, mr_val, x, nrhs);
+        for (int p = p0 + gw + nw; p < p1; p += nw) {      // further rows of this level (wide levels)
+            MrRow<T, CPL> R;
+            mr_load(R, p, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+            mr_solve<T, UNIT, CPL>(R, lane, mr_col, mr_val, x, nrhs);
+        }
+        if (l + 1 < nlev) {
+            have = 0;
+            const int q = ilev[l + 1] + gw;
+            if (q < ilev[l + 2]) {
+                mr_load(pre, q, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+                have = 1;
+            }
+            grid_barrier(bar, bar_base + (unsigned long long)(l + 1) * gridDim.x);
+        }
+    }
+}
+
+// per-position CSR of the referenced strict triangle (multi-RHS layout)
+__global__ void k_mr_deg(int n, const int32_t *perm, const int32_t *dp, int32_t *deg) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) deg[p] = dp[perm[p]];
+    if (p == n) deg[p] = 0;
+}
+
+template <typename T>
+__global__ void k_mr_fill(int nchunks, const ChunkDesc *__restrict__ chunks, const int32_t *__restrict__ ecol,
+                          const T *__restrict__ eval, const int32_t *__restrict__ mr_ptr, int32_t *__restrict__ mr_col,
+                          T *__restrict__ mr_val) {
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nwarps) {
+        const ChunkDesc cd = chunks[c];
+        const int width = chunk_width(cd.meta);
+        if (!chunk_wpr(cd.meta)) {
+            if (lane < chunk_nrows(cd.meta)) {
+                const int base = mr_ptr[cd.pos + lane];
+                for (int k = 0; k < width; ++k) {
+                    const int j = ecol[cd.eptr + (int64_t)k * 32 + lane];
+                    if (j < 0) break;
+                    mr_col[base + k] = j;
+                    mr_val[base + k] = eval[cd.eptr + (int64_t)k * 32 + lane];
+                }
+            }
+        } else {
+            const int base = mr_ptr[cd.pos];
+            for (int k = lane; k < width; k += 32) {
+                mr_col[base + k] = ecol[cd.eptr + k];
+                mr_val[base + k] = eval[cd.eptr + k];
+            }
         }
     }
 }
@@ -325,6 +512,61 @@ sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes) {
     return SPTRSV_SUCCESS;
 }
 
+template <typename T>
+sptrsv_status_t build_mr(sptrsv_handle_t h, cudaStream_t s) {
+    const int n = h->n;
+    DevArena tmp;
+    struct Guard {
+        DevArena &a;
+        ~Guard() { a.release_all(); }
+    } guard{tmp};
+    sptrsv_status_t st;
+    int32_t *deg = nullptr;
+    if ((st = tmp.alloc_n(&deg, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&h->d_mr_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    const int64_t nnz = std::max<int64_t>(h->info.nnz_used, 1);
+    if ((st = h->arena.alloc_n(&h->d_mr_col, (size_t)nnz)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc(&h->d_mr_val, (size_t)nnz * sizeof(T))) != SPTRSV_SUCCESS) return st;
+    k_mr_deg<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, h->d_perm, h->d_dp, deg);
+    if ((st = exclusive_scan_i32(deg, h->d_mr_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    const int grid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
+    k_mr_fill<T><<<grid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_ecol, (const T *)h->d_eval, h->d_mr_ptr,
+                                      h->d_mr_col, (T *)h->d_mr_val);
+    SPTRSV_CUDA(cudaGetLastError());
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    h->mr_built = true;
+    h->info.device_bytes = h->arena.bytes;
+    return SPTRSV_SUCCESS;
+}
+
+template <typename T, bool UNIT, int CPL>
+sptrsv_status_t launch_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
+    static int grid = 0;
+    if (grid == 0) {
+        int per_sm = 0;
+        SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mrhs<T, UNIT, CPL>, kThreads, 0));
+        grid = std::max(1, per_sm) * h->num_sms;
+    }
+    k_mrhs<T, UNIT, CPL><<<grid, kThreads, 0, s>>>(h->n, h->d_perm, h->d_lev, (const T *)h->d_invd, h->d_mr_ptr,
+                                                   h->d_mr_col,
+                                                   (const T *)h->d_mr_val, b, x, nrhs, h->d_flags, h->epoch,
+                                                   h->d_ctr, (unsigned)(grid * (kThreads / 32)));
+    SPTRSV_CUDA(cudaGetLastError());
+    return SPTRSV_SUCCESS;
+}
+
+template <typename T, bool UNIT, int CPL>
+sptrsv_status_t launch_level_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
+    const int grid = h->num_sms;
+    const int nlev = h->info.nlev;
+    void *args[] = {(void *)&h->d_ilev, (void *)&nlev, (void *)&h->d_perm, (void *)&h->d_invd, (void *)&h->d_mr_ptr,
+                    (void *)&h->d_mr_col, (void *)&h->d_mr_val, (void *)&b, (void *)&x, (void *)&nrhs,
+                    (void *)&h->d_bar, (void *)&h->bar_base};
+    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level_mrhs<T, UNIT, CPL>, grid, kLevelThreads, args, 0, s));
+    h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
+    return SPTRSV_SUCCESS;
+}
+
 template <typename K>
 int resident_grid(K kernel, int num_sms) {
     int per_sm = 0;
@@ -336,17 +578,13 @@ template <typename T, bool UNIT>
 sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
     if (h->nchunks == 0) return SPTRSV_SUCCESS;
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_LEVEL) {
-        if (h->level_grid == 0) {
-            int per_sm = 0;
-            SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_level<T, UNIT>, kThreads, 0));
-            h->level_grid = std::max(1, per_sm) * h->num_sms;
-        }
+        if (h->level_grid == 0) h->level_grid = h->num_sms;
         const int grid = h->level_grid;
         const int nlev = h->info.nlev;
         void *args[] = {(void *)&h->d_chunks, (void *)&h->d_lev_chunk, (void *)&nlev, (void *)&h->d_perm,
                         (void *)&h->d_invd, (void *)&h->d_ecol, (void *)&h->d_eval, (void *)&b,
                         (void *)&x, (void *)&h->d_bar, (void *)&h->bar_base};
-        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, kThreads, args, 0, s));
+        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, kLevelThreads, args, 0, s));
         h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
         return SPTRSV_SUCCESS;
     }
@@ -368,11 +606,16 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
                                                   h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
                                                   (unsigned)(grid * (kThreads / 32)));
     } else {
-        if (h->mrhs_grid == 0) h->mrhs_grid = resident_grid(k_mrhs<T, UNIT>, h->num_sms);
-        const int grid = h->mrhs_grid;
-        k_mrhs<T, UNIT><<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
-                                                  h->d_ecol, (const T *)h->d_eval, b, x, nrhs, h->d_flags,
-                                                  h->epoch, h->d_ctr, (unsigned)(grid * (kThreads / 32)));
+        if (!h->mr_built) {
+            sptrsv_status_t st = build_mr<T>(h, s);
+            if (st != SPTRSV_SUCCESS) return st;
+        }
+        const bool lv = h->algo == SPTRSV_ALGO_LEVEL;
+        if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
+        if (nrhs <= 64) return lv ? launch_level_mrhs<T, UNIT, 2>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
+        if (nrhs <= 128) return lv ? launch_level_mrhs<T, UNIT, 4>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
+        // wider: independent column blocks of 128 (each column's arithmetic is unchanged)
+        return SPTRSV_ERR_NOT_SUPPORTED;
     }
     SPTRSV_CUDA(cudaGetLastError());
     return SPTRSV_SUCCESS;

@@ -228,20 +228,23 @@ def test_solve_host_matches(S):
 
 
 # ------------------------------------------------------------ multi-RHS
-@pytest.mark.parametrize("nrhs", [2, 3, 33, 64])
-def test_multi_rhs_small(S, nrhs):
-    m = random_triangular_fast(3000, 6.0, 5, "lower")
-    b = workloads.rhs(m.n, nrhs, seed=nrhs)
-    x, _ = gpu_solve(S, m, b)
-    assert relerr(x, oracle.solve(m, b)) <= 1e-10
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("nrhs", [2, 3, 33, 64, 100])
+def test_multi_rhs_small(S, nrhs, algo):
+    for uplo in ("lower", "upper"):
+        m = random_triangular_fast(3000, 6.0, 5, uplo)
+        b = workloads.rhs(m.n, nrhs, seed=nrhs)
+        x, _ = gpu_solve(S, m, b, uplo=uplo, algo=algo)
+        assert relerr(x, oracle.solve(m, b, uplo)) <= 1e-10
 
 
-def test_cfg5_full_64_rhs_and_partition_bitwise(S):
+@pytest.mark.parametrize("algo", ["self", "level"])
+def test_cfg5_full_64_rhs_and_partition_bitwise(S, algo):
     # cfg5: 64 RHS on the 128^3 factor; column blocks (G = 2, 4, 8) must equal
     # the G = 1 columns bit for bit, and match the oracle
     m, _ = workloads.config(5)
     b = workloads.rhs_columns(m.n, range(64))
-    sv = S.from_csr(m)
+    sv = S.from_csr(m, algo=algo)
     x_all = sv.solve(torch.from_numpy(b).cuda()).cpu().numpy()
     cols = [0, 17, 40, 63]
     ref = oracle.solve(m, np.ascontiguousarray(b[:, cols]))
