@@ -24,13 +24,14 @@
 // processes its levels in increasing order, so the lowest unfinished level
 // always advances.
 //
-// Step records (global, 16-byte aligned), streamed per warp into a shared-memory
+// Step records: one fixed-size record per (warp, level) step of <= 32 rows
+// (lane = row), contiguous per warp, streamed into a per-warp shared-memory
 // ring by TMA bulk copies (cp.async.bulk + mbarrier), nst records in flight:
-//   int4 {p0, nr, w, bytes} | int4 {off_lo, off_hi, bytes, 0} of the record
-//   this warp fetches when it consumes this one | int32 rows[nr] |
-//   int32 cols[w][nr] | T invd[nr] | T vals[w][nr]   (arrays padded to 16 B)
-//   cols >= 0: global column; cols < 0: shared slot -1-cols (the warp's
-//   zero slot pads short rows).  Entries beyond kTprMax: ovf_* (CSR by position).
+//   int32 rows[32] (-1 = padding lane) | int32 cols[W][32] | T invd[32] | T vals[W][32]
+//   cols >= 0: global column (another CTA, or a value that left the ring);
+//   cols < 0: shared slot -1-cols (slot Z = the zero slot pads short rows).
+//   W = min(max dependencies per row, kTprMax); the rest: ovf_* (CSR by position).
+// Every per-step address is a constant offset, so the step loop is short.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -43,18 +44,19 @@ namespace {
 
 constexpr int kWPC = 4;          // warps (tiles) per CTA
 constexpr int kBuckets = kTprMax + 2;
-constexpr int kAheadB = 6;       // lead of the b loads (steps)
-constexpr int kAheadX = 2;       // lead of the speculative external x loads
-constexpr int kBRing = kAheadB + 2;   // per-warp shared ring of b values [kBRing][32]
-constexpr int kXRing = kAheadX + 2;   // per-warp shared ring of speculative x [kXRing][MAXW][32]
-constexpr int kMinStages = 8;    // records in flight per warp (> kAheadB + 1, or the lookahead deadlocks)
-static_assert(kMinStages >= kAheadB + 2 && kMinStages >= kAheadX + 2, "record ring shorter than the lookahead");
+constexpr int kLead = 2;         // register lead of b / speculative external x (3 register sets)
+constexpr int kPrefB = 6;        // L2 prefetch lead of b
+constexpr int kSleepSmemNs = 40;    // poll back-off: a spinning warp must not starve its SM's LSU pipe
+constexpr int kSleepGlobalNs = 80;
+constexpr int kMinStages = 8;    // records in flight per warp (> kPrefB, or the lookahead deadlocks)
+static_assert(kMinStages > kPrefB && kMinStages > kLead + 1, "record ring shorter than the lookahead");
 
 __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax ? 0u : (uint32_t)(kTprMax + 1 - deps); }
-__host__ __device__ __forceinline__ int64_t a16(int64_t v) { return (v + 15) & ~(int64_t)15; }
-__host__ __device__ __forceinline__ int64_t rec_bytes(int nr, int w, int es) {
-    return 32 + a16(4ll * nr) + a16(4ll * w * nr) + a16((int64_t)es * nr) + a16((int64_t)es * w * nr);
-}
+// fixed record geometry: rows | cols[W] | invd | vals[W], 32 lanes each
+__host__ __device__ __forceinline__ int rec_bytes(int W, int es) { return 32 * (4 + 4 * W + es + es * W); }
+__host__ __device__ __forceinline__ int rec_cols(int) { return 32 * 4; }
+__host__ __device__ __forceinline__ int rec_invd(int W) { return 32 * 4 * (1 + W); }
+__host__ __device__ __forceinline__ int rec_vals(int W, int es) { return 32 * (4 * (1 + W) + es); }
 
 // -------------------------------------------------------------- build kernels
 // natural-order CSR of the referenced strict triangle, from the chunk layout
@@ -104,7 +106,8 @@ __global__ void k_grid_check(int n, int nx, int ny, const int32_t *__restrict__ 
     if (!ok) atomicAdd(bad, 1u);
 }
 
-// (x, y) tiles: CTA (cx, cy) owns the 2x2 tiles (2cx..2cx+1, 2cy..2cy+1)
+// (x, y) tiles: CTA (cx, cy) owns the 2x2 tiles (2cx..2cx+1, 2cy..2cy+1);
+// a tile is a set of z-columns, so the z-chains stay inside one warp
 __global__ void k_part_tiles(int n, int nx, int ny, int cxn, int cyn, int32_t *unit) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -127,15 +130,13 @@ __global__ void k_unit_keys(int n, int nlev, const int32_t *unit, const int32_t 
     if (i < n) keys[i] = ((uint32_t)unit[i] * (uint32_t)nlev + (uint32_t)lev[i]) * kBuckets + bucket_of(dp[i]);
 }
 
-// head flags of groups (new (unit, level)); inverse permutation; unit sizes
-__global__ void k_heads(const uint32_t *skeys, const int32_t *bperm, const int32_t *unit, int n, int32_t *head,
-                        int32_t *pos, int32_t *unit_rows) {
+// head flags of groups (new (unit, level)); inverse permutation
+__global__ void k_heads(const uint32_t *skeys, const int32_t *bperm, int n, int32_t *head, int32_t *pos) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const uint32_t s = skeys[p] / kBuckets;
     head[p] = (p == 0 || skeys[p - 1] / kBuckets != s) ? 1 : 0;
     pos[bperm[p]] = p;
-    atomicAdd(&unit_rows[unit[bperm[p]]], 1);
 }
 
 __global__ void k_group_start(const int32_t *head, const int32_t *gid, int n, int ngroups, int32_t *gp0) {
@@ -144,28 +145,24 @@ __global__ void k_group_start(const int32_t *head, const int32_t *gid, int n, in
     if (p == 0) gp0[ngroups] = n;
 }
 
-__global__ void k_group_sub(const int32_t *gp0, int ngroups, int rc, int32_t *nsub) {
+__global__ void k_group_sub(const int32_t *gp0, int ngroups, int32_t *nsub) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g < ngroups) nsub[g] = (gp0[g + 1] - gp0[g] + rc - 1) / rc;
+    if (g < ngroups) nsub[g] = (gp0[g + 1] - gp0[g] + 31) / 32;
     if (g == ngroups) nsub[g] = 0;
 }
 
-// per group: its 32-row sub-steps {p0, nr, w}; unit of each step
-__global__ void k_steps(const int32_t *gp0, const int32_t *sub0, int ngroups, int rc, const int32_t *bperm,
-                        const int32_t *dp, const int32_t *unit, int4 *steps, int32_t *step_unit, int *maxw) {
+// per group: its 32-row steps (first position, rows); unit of each step
+__global__ void k_steps(const int32_t *gp0, const int32_t *sub0, int ngroups, const int32_t *bperm,
+                        const int32_t *unit, int2 *steps, int32_t *step_unit) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= ngroups) return;
     const int a = gp0[g], e = gp0[g + 1];
     int s = sub0[g];
     const int u = unit[bperm[a]];
-    int wmax = 0;
-    for (int p0 = a; p0 < e; p0 += rc, ++s) {
-        const int w = min(dp[bperm[p0]], kTprMax);      // first row has the most deps
-        steps[s] = make_int4(p0, min(rc, e - p0), w, 0);
+    for (int p0 = a; p0 < e; p0 += 32, ++s) {
+        steps[s] = make_int2(p0, min(32, e - p0));
         step_unit[s] = u;
-        wmax = max(wmax, w);
     }
-    atomicMax(maxw, wmax);
 }
 
 __global__ void k_unit_step0(const int32_t *step_unit, int nsteps, int U, int32_t *unit_step0) {
@@ -178,129 +175,90 @@ __global__ void k_unit_step0(const int32_t *step_unit, int nsteps, int U, int32_
         for (int uu = step_unit[s] + 1; uu <= U; ++uu) unit_step0[uu] = nsteps;
 }
 
-__global__ void k_rec_sizes(const int4 *steps, int nsteps, int es, int64_t *rb, int *rec_max) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s < nsteps) {
-        const int64_t v = rec_bytes(steps[s].y, steps[s].z, es);
-        rb[s] = v;
-        atomicMax(rec_max, (int)v);
-    }
-    if (s == nsteps) rb[s] = 0;
-}
-
-__global__ void k_pos_step(const int32_t *head, const int32_t *gid, const int32_t *gp0, const int32_t *sub0, int n,
-                           int rc, int32_t *step_of) {
+// position -> step; padded position of each row inside its warp's step stream
+__global__ void k_pos_step(const int32_t *head, const int32_t *gid, const int32_t *gp0, const int32_t *sub0,
+                           const int2 *steps, const int32_t *bperm, const int32_t *unit,
+                           const int32_t *unit_step0, int n, int32_t *step_of, int32_t *ppos) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int g = gid[p] + head[p] - 1;
-    step_of[p] = sub0[g] + (p - gp0[g]) / rc;
+    const int s = sub0[g] + (p - gp0[g]) / 32;
+    step_of[p] = s;
+    const int row = bperm[p];
+    ppos[row] = (s - unit_step0[unit[row]]) * 32 + (p - steps[s].x);
 }
 
-__global__ void k_ovf_count(int n, const int32_t *bperm, const int32_t *dp, int32_t *ocnt) {
+__global__ void k_ovf_count(int n, const int32_t *bperm, const int32_t *dp, int W, int32_t *ocnt) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) ocnt[p] = max(0, dp[bperm[p]] - kTprMax);
+    if (p < n) ocnt[p] = max(0, dp[bperm[p]] - W);
     if (p == n) ocnt[p] = 0;
 }
 
-// slot of a produced value: warp-local ring of Wu (power of two) slots
-__host__ __device__ __forceinline__ int slot_index(int u, int local, int Wu) {
-    return (u % kWPC) * (Wu + 1) + (local & (Wu - 1));
+// padding lanes of every step: row -1, zero-slot columns, zero values
+template <typename T>
+__global__ void k_rec_pad(int nsteps, int W, int Z, const int2 *steps, unsigned char *recs) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)nsteps * 32) return;
+    const int s = (int)(t >> 5), lane = (int)(t & 31);
+    if (lane < steps[s].y) return;
+    unsigned char *base = recs + (size_t)s * rec_bytes(W, sizeof(T));
+    reinterpret_cast<int32_t *>(base)[lane] = -1;
+    int32_t *cols = reinterpret_cast<int32_t *>(base + rec_cols(W));
+    T *vals = reinterpret_cast<T *>(base + rec_vals(W, sizeof(T)));
+    for (int k = 0; k < W; ++k) {
+        cols[k * 32 + lane] = -1 - Z;
+        vals[k * 32 + lane] = T(0);
+    }
+    reinterpret_cast<T *>(base + rec_invd(W))[lane] = T(0);
 }
 
 template <typename T>
-__global__ void k_rec_fill(int n, int Wu, int nst, const int32_t *__restrict__ unit,
-                           const int32_t *__restrict__ unit_rows, const int32_t *__restrict__ step_of,
-                           const int32_t *__restrict__ bperm, const int32_t *__restrict__ pos,
-                           const int4 *__restrict__ steps, const int64_t *__restrict__ rec_off,
-                           const int32_t *__restrict__ unit_step0, const int32_t *__restrict__ tri_ptr,
+__global__ void k_rec_fill(int n, int Wu, int W, int Z, const int32_t *__restrict__ unit,
+                           const int32_t *__restrict__ unit_step0, const int32_t *__restrict__ step_of,
+                           const int32_t *__restrict__ bperm, const int32_t *__restrict__ ppos,
+                           const int2 *__restrict__ steps, const int32_t *__restrict__ tri_ptr,
                            const int32_t *__restrict__ tri_col, const T *__restrict__ tri_val,
                            const T *__restrict__ invd_row, const int32_t *__restrict__ ovf_ptr,
                            unsigned char *__restrict__ recs, int32_t *__restrict__ ovf_col, T *__restrict__ ovf_val) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int s = step_of[p];
-    const int4 st = steps[s];
-    const int nr = st.y, w = st.z, j = p - st.x;
-    unsigned char *base = recs + rec_off[s];
+    const int lane = p - steps[s].x;
     const int row = bperm[p];
     const int u = unit[row];
-    if (j == 0) {
-        *reinterpret_cast<int4 *>(base) = make_int4(st.x, nr, w, (int)(rec_off[s + 1] - rec_off[s]));
-        const int sn = s + nst - 1;
-        int4 nx = make_int4(0, 0, 0, 0);
-        if (sn < unit_step0[u + 1]) {
-            const int64_t off = rec_off[sn];
-            nx = make_int4((int)(off & 0xffffffffll), (int)(off >> 32), (int)(rec_off[sn + 1] - off), 0);
-        }
-        *reinterpret_cast<int4 *>(base + 16) = nx;
-    }
-    unsigned char *q = base + 32;
-    int32_t *rows = reinterpret_cast<int32_t *>(q);
-    q += a16(4ll * nr);
-    int32_t *cols = reinterpret_cast<int32_t *>(q);
-    q += a16(4ll * w * nr);
-    T *invd = reinterpret_cast<T *>(q);
-    q += a16((int64_t)sizeof(T) * nr);
-    T *vals = reinterpret_cast<T *>(q);
-    rows[j] = row;
-    invd[j] = invd_row[row];
-    const int u_p0 = steps[unit_step0[u]].x;
-    const int step_end_local = st.x + nr - u_p0;
+    unsigned char *base = recs + (size_t)s * rec_bytes(W, sizeof(T));
+    reinterpret_cast<int32_t *>(base)[lane] = row;
+    reinterpret_cast<T *>(base + rec_invd(W))[lane] = invd_row[row];
+    int32_t *cols = reinterpret_cast<int32_t *>(base + rec_cols(W));
+    T *vals = reinterpret_cast<T *>(base + rec_vals(W, sizeof(T)));
+    const int step_end_pp = (s - unit_step0[u] + 1) * 32;        // padded end of the consumer's step
     int k = 0;
     for (int kk = tri_ptr[row]; kk < tri_ptr[row + 1]; ++kk, ++k) {
-        const int jj = tri_col[kk];
-        const int uj = unit[jj];
-        int code = jj;                                   // global (another CTA, or left the ring)
+        const int j = tri_col[kk];
+        const int uj = unit[j];
+        int code = j;                                    // global: another CTA, or left the ring
         if (uj / kWPC == u / kWPC) {
-            const int pj = pos[jj];
-            const int uj_p0 = steps[unit_step0[uj]].x;
-            const int lj = pj - uj_p0;
-            if (uj == u) {
-                if (lj + Wu >= step_end_local) code = -1 - slot_index(uj, lj, Wu);
-            } else if (unit_rows[uj] <= Wu) {            // no slot reuse in the producer warp
-                code = -1 - slot_index(uj, lj, Wu);
-            }
+            const int pj = ppos[j];
+            const bool ring_ok = (uj == u) ? (pj + Wu >= step_end_pp)            // overwritten later than now
+                                           : ((unit_step0[uj + 1] - unit_step0[uj]) * 32 <= Wu);   // never overwritten
+            if (ring_ok) code = -1 - ((uj % kWPC) * Wu + (pj & (Wu - 1)));
         }
-        if (k < w) {
-            cols[k * nr + j] = code;
-            vals[k * nr + j] = tri_val[kk];
+        if (k < W) {
+            cols[k * 32 + lane] = code;
+            vals[k * 32 + lane] = tri_val[kk];
         } else {
-            const int o = ovf_ptr[p] + (k - w);
+            const int o = ovf_ptr[p] + (k - W);
             ovf_col[o] = code;
             ovf_val[o] = tri_val[kk];
         }
     }
-    for (; k < w; ++k) {
-        cols[k * nr + j] = -1 - ((u % kWPC) * (Wu + 1) + Wu);    // the warp's zero slot
-        vals[k * nr + j] = T(0);
+    for (; k < W; ++k) {
+        cols[k * 32 + lane] = -1 - Z;
+        vals[k * 32 + lane] = T(0);
     }
 }
 
 // ------------------------------------------------------------------ solve
-template <typename T>
-struct RecView {
-    int4 hdr;
-    int4 nxt;
-    const int32_t *rows;
-    const int32_t *cols;
-    const T *invd;
-    const T *vals;
-    RecView() = default;
-    __device__ __forceinline__ RecView(const unsigned char *base) {
-        hdr = *reinterpret_cast<const int4 *>(base);
-        nxt = *reinterpret_cast<const int4 *>(base + 16);
-        const int nr = hdr.y, w = hdr.z;
-        const unsigned char *q = base + 32;
-        rows = reinterpret_cast<const int32_t *>(q);
-        q += a16(4ll * nr);
-        cols = reinterpret_cast<const int32_t *>(q);
-        q += a16(4ll * w * nr);
-        invd = reinterpret_cast<const T *>(q);
-        q += a16((int64_t)sizeof(T) * nr);
-        vals = reinterpret_cast<const T *>(q);
-    }
-};
-
 __device__ __forceinline__ double lds_volatile(const double *p) {
     double v;
     asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
@@ -330,28 +288,26 @@ __device__ __noinline__ bool wd_expired(unsigned long long t0) {
 }
 
 template <typename T>
-__device__ __forceinline__ T poll_smem(const T *p) {
+__device__ __noinline__ T poll_smem_slow(const T *p) {
+    const unsigned long long t0 = wd_now();
     T v = lds_volatile(p);
-    if (Sentinel<T>::is(v)) {
-        const unsigned long long t0 = wd_now();
-        unsigned it = 0;
-        while (Sentinel<T>::is(v)) {
-            v = lds_volatile(p);
-            if ((++it & 4095u) == 0 && wd_expired(t0)) break;
-        }
+    unsigned it = 0;
+    while (Sentinel<T>::is(v)) {
+        __nanosleep(kSleepSmemNs);       // leave the shared-memory pipe to the working warps
+        v = lds_volatile(p);
+        if ((++it & 1023u) == 0 && wd_expired(t0)) break;
     }
     return v;
 }
 template <typename T>
-__device__ __forceinline__ T poll_global(const T *p, T v) {
-    if (Sentinel<T>::is(v)) {
-        const unsigned long long t0 = wd_now();
-        unsigned it = 0;
-        while (Sentinel<T>::is(v)) {
-            __nanosleep(8);
-            v = ld_relaxed_val(p);
-            if ((++it & 1023u) == 0 && wd_expired(t0)) break;
-        }
+__device__ __noinline__ T poll_global_slow(const T *p) {
+    const unsigned long long t0 = wd_now();
+    T v = ld_relaxed_val(p);
+    unsigned it = 0;
+    while (Sentinel<T>::is(v)) {
+        __nanosleep(kSleepGlobalNs);
+        v = ld_relaxed_val(p);
+        if ((++it & 1023u) == 0 && wd_expired(t0)) break;
     }
     return v;
 }
@@ -360,44 +316,41 @@ __device__ __forceinline__ T poll_global(const T *p, T v) {
 // records %globaltimer at its first `cap` - 1 steps and at the end.
 __device__ unsigned long long *g_trace = nullptr;
 __device__ int g_trace_cap = 0;
-__device__ unsigned long long *g_phase = nullptr;     // TRACE build: warp 0, 4 clock64 stamps x 128 steps
-
+__device__ unsigned long long *g_phase = nullptr;     // TRACE build: warp 0, 5 clock64 stamps x 128 steps
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 
-// Register state of one step, loaded two steps ahead (record view, b, and
-// the speculative external x).  The loop is unrolled by two over two such
-// sets, so no register is ever moved and no load latency lands on the step.
 template <typename T, int MAXW>
-struct StepRegs {
-    RecView<T> r;
+struct Lead {
+    int row;
     T bv;
     T xv[MAXW];
 };
 
-// Per warp, per step s (lane = row of the step):
-//   lookahead  record s+2 (wait), issue b and speculative external x loads of
-//              step s+2 into the other register set; L2-prefetch b of step
-//              s+6 if its record has landed; lane 0 refills the record ring;
-//   solve      deps from shared slots (polled) or the speculative value
-//              (re-polled from L2 only if still the sentinel); FMA chain;
-//              result to this warp's slot and to x; __syncwarp.
+// One warp = one tile of rows; lane = row of the current step.  Per step s:
+//   lead   (record s+2 is here) row, b and the speculative external x of step
+//          s+2 into a register set; 3 sets rotate by unrolling, never by moves;
+//   ring   lane 0 refills the record ring (TMA, record s+nst-1); b of step
+//          s+6 is prefetched into L2 if its record has landed;
+//   solve  deps from shared slots (polled: written by this warp before the
+//          last __syncwarp, or by a neighbour warp) or the speculative value
+//          (re-polled from L2 only if it was still the sentinel); FMA chain;
+//          result to the warp's slot and to x; __syncwarp.
 template <typename T, bool UNIT, int MAXW, bool TRACE>
 __global__ void __launch_bounds__(32 * kWPC, 1)
-    k_block(int Wu, int nst, int rec_max, const int32_t *__restrict__ unit_step0, const int64_t *__restrict__ rec_off,
-            const unsigned char *__restrict__ recs, const int32_t *__restrict__ ovf_ptr,
-            const int32_t *__restrict__ ovf_col, const T *__restrict__ ovf_val, const T *b, T *x) {
+    k_block(int Wu, int W, int nst, const int32_t *__restrict__ unit_step0, const unsigned char *__restrict__ recs,
+            const int32_t *__restrict__ ovf_ptr, const int32_t *__restrict__ ovf_col,
+            const T *__restrict__ ovf_val, const int32_t *__restrict__ ovf_pos, const T *b, T *x) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int REC = rec_bytes(W, sizeof(T));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw) + warp * nst;
-    unsigned char *ring = smem_raw + 8 * (size_t)kWPC * nst + (size_t)warp * nst * rec_max;
-    T *xs = reinterpret_cast<T *>(smem_raw + 8 * (size_t)kWPC * nst + (size_t)kWPC * nst * rec_max);
-    // sentinel-prefill every slot (zero slot = 0), then make it CTA-visible
-    for (int i = threadIdx.x; i < kWPC * (Wu + 1); i += blockDim.x)
-        xs[i] = (i % (Wu + 1) == Wu) ? T(0) : Sentinel<T>::value();
+    unsigned char *ring = smem_raw + 8 * (size_t)kWPC * nst + (size_t)warp * nst * REC;
+    T *xs = reinterpret_cast<T *>(smem_raw + 8 * (size_t)kWPC * nst + (size_t)kWPC * nst * REC);
+    for (int i = threadIdx.x; i <= kWPC * Wu; i += blockDim.x) xs[i] = (i == kWPC * Wu) ? T(0) : Sentinel<T>::value();
     const int u = blockIdx.x * kWPC + warp;
     const int s0 = unit_step0[u], s1 = unit_step0[u + 1];
     if (lane == 0) {
@@ -406,12 +359,15 @@ __global__ void __launch_bounds__(32 * kWPC, 1)
     }
     __syncthreads();
     if (s0 == s1) return;
-    auto issue_at = [&](int s, int64_t off, uint32_t bytes) {     // lane 0 only
-        const int slot = (s - s0) & (nst - 1);
-        mbar_arrive_expect_tx(&bars[slot], bytes);
-        bulk_g2s(ring + (size_t)slot * rec_max, recs + off, bytes, &bars[slot]);
+    T *myslots = xs + warp * Wu;
+    const int cW = rec_cols(W), iW = rec_invd(W), vW = rec_vals(W, sizeof(T));
+    auto slot_of = [&](int s) { return ring + (size_t)((s - s0) & (nst - 1)) * REC; };
+    auto issue = [&](int s) {     // lane 0
+        uint64_t *bar = &bars[(s - s0) & (nst - 1)];
+        mbar_arrive_expect_tx(bar, (uint32_t)REC);
+        bulk_g2s(slot_of(s), recs + (size_t)s * REC, (uint32_t)REC, bar);
     };
-    auto wait_rec = [&](int s) {
+    auto wait = [&](int s) {
         const int i = s - s0;
         uint64_t *bar = &bars[i & (nst - 1)];
         const uint32_t par = (uint32_t)((i / nst) & 1);
@@ -420,87 +376,96 @@ __global__ void __launch_bounds__(32 * kWPC, 1)
             while (!mbar_try_wait(bar, par))
                 if (wd_expired(t0)) break;
         }
-        return RecView<T>(ring + (size_t)(i & (nst - 1)) * rec_max);
     };
-    auto load_regs = [&](StepRegs<T, MAXW> &R, int s) {
-        R.r = wait_rec(s);
-        if (lane < R.r.hdr.y) {
-            R.bv = ld_cg(b + R.r.rows[lane]);
+    auto lead = [&](Lead<T, MAXW> &L, int s) {          // record s has landed
+        const unsigned char *r = slot_of(s);
+        L.row = reinterpret_cast<const int32_t *>(r)[lane];
+        if (L.row >= 0) L.bv = ld_cg(b + L.row);
+        const int32_t *cols = reinterpret_cast<const int32_t *>(r + cW);
 #pragma unroll
-            for (int k = 0; k < MAXW; ++k) {
-                if (k < R.r.hdr.z) {
-                    const int c = R.r.cols[k * R.r.hdr.y + lane];
-                    if (c >= 0) R.xv[k] = ld_relaxed_val(x + c);
-                }
+        for (int k = 0; k < MAXW; ++k) {
+            if (k < W) {
+                const int c = cols[k * 32 + lane];
+                if (c >= 0) L.xv[k] = ld_relaxed_val(x + c);
             }
         }
     };
-    auto prefetch_b = [&](int s) {      // L2 warm-up of b, only if the record already landed
-        const int i = s - s0;
-        if (mbar_test_wait(&bars[i & (nst - 1)], (uint32_t)((i / nst) & 1))) {
-            const unsigned char *base = ring + (size_t)(i & (nst - 1)) * rec_max;
-            const int nr = reinterpret_cast<const int4 *>(base)->y;
-            if (lane < nr) prefetch_l2(b + reinterpret_cast<const int32_t *>(base + 32)[lane]);
-        }
-    };
-    if (lane == 0)
-        for (int s = s0; s < min(s1, s0 + nst - 1); ++s) issue_at(s, rec_off[s], (uint32_t)(rec_off[s + 1] - rec_off[s]));
-    const int u_p0 = wait_rec(s0).hdr.x;
-    auto solve = [&](StepRegs<T, MAXW> &R, int s) {
-        const RecView<T> &r = R.r;
-        if (lane == 0 && r.nxt.z != 0) {
-            // slot (s-1) % nst: every lane finished reading it before the last __syncwarp
-            issue_at(s + nst - 1, (int64_t)(uint32_t)r.nxt.x | ((int64_t)r.nxt.y << 32), (uint32_t)r.nxt.z);
-        }
-        const int nr = r.hdr.y, w = r.hdr.z;
-        if (lane < nr) {
-            T acc = R.bv;
+    auto solve = [&](const Lead<T, MAXW> &L, int s) {
+        const unsigned char *r = slot_of(s);
+        if (L.row >= 0) {
+            const int32_t *cols = reinterpret_cast<const int32_t *>(r + cW);
+            const T *vals = reinterpret_cast<const T *>(r + vW);
+            T acc = L.bv;
 #pragma unroll
             for (int k = 0; k < MAXW; ++k) {
-                if (k < w) {
-                    const int c = r.cols[k * nr + lane];
-                    const T v = c < 0 ? poll_smem(xs - 1 - c) : poll_global(x + c, R.xv[k]);
-                    acc = fnma(r.vals[k * nr + lane], v, acc);
+                if (k < W) {
+                    const int c = cols[k * 32 + lane];
+                    T v;
+                    if (c < 0) {
+                        v = lds_volatile(xs - 1 - c);
+                        if (Sentinel<T>::is(v)) v = poll_smem_slow(xs - 1 - c);
+                    } else {
+                        v = L.xv[k];
+                        if (Sentinel<T>::is(v)) v = poll_global_slow(x + c);
+                    }
+                    acc = fnma(vals[k * 32 + lane], v, acc);
                 }
             }
-            const int p = r.hdr.x + lane;
-            if (MAXW >= kTprMax && w == kTprMax) {
+            if (MAXW >= kTprMax && W == kTprMax) {
+                const int p = ovf_pos[L.row];
                 for (int o = ovf_ptr[p]; o < ovf_ptr[p + 1]; ++o) {
                     const int c = ovf_col[o];
-                    const T v = c < 0 ? poll_smem(xs - 1 - c) : poll_global(x + c, ld_relaxed_val(x + c));
+                    T v = c < 0 ? lds_volatile(xs - 1 - c) : ld_relaxed_val(x + c);
+                    if (Sentinel<T>::is(v)) v = c < 0 ? poll_smem_slow(xs - 1 - c) : poll_global_slow(x + c);
                     acc = fnma(ovf_val[o], v, acc);
                 }
             }
-            const T res = Sentinel<T>::scrub(UNIT ? acc : acc * r.invd[lane]);
-            xs[slot_index(u, p - u_p0, Wu)] = res;
-            st_relaxed_val(x + r.rows[lane], res);
+            const T res = Sentinel<T>::scrub(UNIT ? acc : acc * reinterpret_cast<const T *>(r + iW)[lane]);
+            myslots[(((s - s0) << 5) + lane) & (Wu - 1)] = res;
+            st_relaxed_val(x + L.row, res);
         }
         __syncwarp();
     };
-    // three register sets with fixed roles in a 3x unrolled loop (lead 2, no moves)
-    StepRegs<T, MAXW> X0, X1, X2;
-    load_regs(X0, s0);
-    if (s0 + 1 < s1) load_regs(X1, s0 + 1);
-#define SPTRSV_BLOCK_STEP(CUR, NXT, OFF)                                                              \
-    {                                                                                                 \
-        const int ss = s + (OFF);                                                                     \
-        if (ss >= s1) break;                                                                          \
-        if (TRACE && lane == 0 && ss - s0 < g_trace_cap - 1)                                          \
-            g_trace[(size_t)u * g_trace_cap + (ss - s0)] = gtimer();                                  \
-        unsigned long long *ph = (TRACE && g_phase && u == 0 && lane == 0 && ss - s0 < 128)            \
-                                     ? g_phase + 4 * (ss - s0) : nullptr;                             \
-        if (ph) ph[0] = clock64();                                                                    \
-        if (ss + 2 < s1) load_regs(NXT, ss + 2);                                                      \
-        if (ph) ph[1] = clock64();                                                                    \
-        if (ss + 6 < s1) prefetch_b(ss + 6);                                                          \
-        if (ph) ph[2] = clock64();                                                                    \
-        solve(CUR, ss);                                                                               \
-        if (ph) ph[3] = clock64();                                                                    \
+    if (lane == 0)
+        for (int s = s0; s < min(s1, s0 + nst - 1); ++s) issue(s);
+    Lead<T, MAXW> L0, L1, L2;
+    wait(s0);
+    lead(L0, s0);
+    if (s0 + 1 < s1) {
+        wait(s0 + 1);
+        lead(L1, s0 + 1);
+    }
+#define SPTRSV_BLOCK_STEP(CUR, NXT, OFF)                                                        \
+    {                                                                                           \
+        const int ss = s + (OFF);                                                               \
+        if (ss >= s1) break;                                                                    \
+        if (TRACE && lane == 0 && ss - s0 < g_trace_cap - 1)                                    \
+            g_trace[(size_t)u * g_trace_cap + (ss - s0)] = gtimer();                            \
+        unsigned long long *ph = (TRACE && g_phase && u == 0 && lane == 0 && ss - s0 < 128)     \
+                                     ? g_phase + 5 * (ss - s0) : nullptr;                       \
+        if (ph) ph[0] = clock64();                                                              \
+        if (ss + kLead < s1) {                                                                  \
+            wait(ss + kLead);                                                                   \
+            if (ph) ph[1] = clock64();                                                          \
+            lead(NXT, ss + kLead);                                                              \
+        }                                                                                       \
+        if (ph) ph[2] = clock64();                                                              \
+        if (lane == 0 && ss + nst - 1 < s1) issue(ss + nst - 1);                                \
+        if (ph) ph[3] = clock64();                                                              \
+        if (ss + kPrefB < s1) {                                                                 \
+            const int i6 = ss + kPrefB - s0;                                                    \
+            if (mbar_test_wait(&bars[i6 & (nst - 1)], (uint32_t)((i6 / nst) & 1))) {            \
+                const int rw = reinterpret_cast<const int32_t *>(slot_of(ss + kPrefB))[lane];   \
+                if (rw >= 0) prefetch_l2(b + rw);                                               \
+            }                                                                                   \
+        }                                                                                       \
+        solve(CUR, ss);                                                                         \
+        if (ph) ph[4] = clock64();                                                              \
     }
     for (int s = s0; s < s1; s += 3) {
-        SPTRSV_BLOCK_STEP(X0, X2, 0)
-        SPTRSV_BLOCK_STEP(X1, X0, 1)
-        SPTRSV_BLOCK_STEP(X2, X1, 2)
+        SPTRSV_BLOCK_STEP(L0, L2, 0)
+        SPTRSV_BLOCK_STEP(L1, L0, 1)
+        SPTRSV_BLOCK_STEP(L2, L1, 2)
     }
 #undef SPTRSV_BLOCK_STEP
     if (TRACE && lane == 0) g_trace[(size_t)u * g_trace_cap + min(s1 - s0, g_trace_cap - 1)] = gtimer();
@@ -519,14 +484,14 @@ int env_int(const char *name, int dflt) {
 }
 
 template <typename T, bool UNIT>
-void *pick_kernel(int maxw, bool trace) {
+void *pick_kernel(int W, bool trace) {
     if (trace) {
-        if (maxw <= 4) return (void *)k_block<T, UNIT, 4, true>;
-        if (maxw <= 8) return (void *)k_block<T, UNIT, 8, true>;
+        if (W <= 4) return (void *)k_block<T, UNIT, 4, true>;
+        if (W <= 8) return (void *)k_block<T, UNIT, 8, true>;
         return (void *)k_block<T, UNIT, kTprMax, true>;
     }
-    if (maxw <= 4) return (void *)k_block<T, UNIT, 4, false>;
-    if (maxw <= 8) return (void *)k_block<T, UNIT, 8, false>;
+    if (W <= 4) return (void *)k_block<T, UNIT, 4, false>;
+    if (W <= 8) return (void *)k_block<T, UNIT, 8, false>;
     return (void *)k_block<T, UNIT, kTprMax, false>;
 }
 bool g_host_trace = false;
@@ -629,27 +594,41 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     // ---- 2. partition rows over U = K x kWPC warps of K co-resident CTAs
     int32_t *unit = nullptr;
     if ((st = tmp.alloc_n(&unit, n)) != SPTRSV_SUCCESS) return st;
-    int K = env_int("SPTRSV_BLOCK_K", 0);
+    int Kmax = env_int("SPTRSV_BLOCK_K", 0);
     const int min_rows = env_int("SPTRSV_BLOCK_MIN_ROWS", 8192);
-    if (K <= 0) K = (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, n / std::max(1, min_rows)));
-    K = std::min(K, h->num_sms);
+    if (Kmax <= 0) Kmax = (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, n / std::max(1, min_rows)));
+    Kmax = std::min(Kmax, h->num_sms);
+    int K = Kmax;
     int gnx = 0, gny = 0;
-    if (K > 1 && !env_int("SPTRSV_BLOCK_NO_GRID", 0)) {
+    if (Kmax > 1 && !env_int("SPTRSV_BLOCK_NO_GRID", 0)) {
         if ((st = detect_grid(h, tri_ptr, tri_col, tmp, s, gnx, gny)) != SPTRSV_SUCCESS) return st;
     }
     if (gnx > 0) {
-        // cxn x cyn CTAs (each 2x2 tiles), tiles of aspect ~1
-        const int cxn = std::max(1, std::min(gnx / 2, (int)std::sqrt((double)K * gnx / gny)));
-        const int cyn = std::max(1, std::min(gny / 2, K / cxn));
-        if (2 * cxn > gnx || 2 * cyn > gny) {
+        // CTA grid cxn x cyn (2x2 tiles each): prefer tiles of <= 32 columns (one
+        // step per level), then more CTAs, then square tiles
+        int best = -1, bcx = 0, bcy = 0;
+        double bscore = -1e30;
+        for (int cx = 1; cx <= std::min(Kmax, gnx / 2); ++cx)
+            for (int cy = 1; cy <= std::min(Kmax / cx, gny / 2); ++cy) {
+                const int tw = (gnx + 2 * cx - 1) / (2 * cx), th = (gny + 2 * cy - 1) / (2 * cy);
+                const bool fits = tw * th <= 32;
+                const double score = (fits ? 1e6 : 0.0) + cx * cy * 10.0 - std::fabs(std::log((double)tw / th));
+                if (score > bscore) {
+                    bscore = score;
+                    best = 1;
+                    bcx = cx;
+                    bcy = cy;
+                }
+            }
+        if (best < 0) {
             gnx = 0;
         } else {
-            K = cxn * cyn;
-            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, cxn, cyn, unit);
+            K = bcx * bcy;
+            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, bcx, bcy, unit);
             B.grid_nx = gnx;
             B.grid_ny = gny;
-            B.tiles_x = 2 * cxn;
-            B.tiles_y = 2 * cyn;
+            B.tiles_x = 2 * bcx;
+            B.tiles_y = 2 * bcy;
         }
     }
     const int U = K * kWPC;
@@ -661,127 +640,111 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
 
     // ---- 3. order (unit, level, decreasing deps, row); groups (unit, level) -> 32-row steps
     uint32_t *keys = nullptr, *skeys = nullptr;
-    int32_t *pos = nullptr, *head = nullptr, *gid = nullptr, *bperm = nullptr, *unit_rows = nullptr;
+    int32_t *pos = nullptr, *head = nullptr, *gid = nullptr, *bperm = nullptr;
     if ((st = tmp.alloc_n(&keys, n)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&skeys, n)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&pos, n)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&head, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&gid, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&bperm, n)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&unit_rows, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(unit_rows, 0, sizeof(int32_t) * ((size_t)U + 1), s));
     k_unit_keys<<<eg, 256, 0, s>>>(n, nlev, unit, h->d_lev, h->d_dp, keys);
     if ((st = radix_sort_pairs(keys, nullptr, skeys, bperm, n, (uint32_t)((uint64_t)U * nlev * kBuckets - 1), tmp,
                                s)) != SPTRSV_SUCCESS)
         return st;
     SPTRSV_CUDA(cudaMemsetAsync(head + n, 0, sizeof(int32_t), s));
-    k_heads<<<eg, 256, 0, s>>>(skeys, bperm, unit, n, head, pos, unit_rows);
+    k_heads<<<eg, 256, 0, s>>>(skeys, bperm, n, head, pos);
     if ((st = exclusive_scan_i32(head, gid, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     int32_t ngroups = 0;
     SPTRSV_CUDA(cudaMemcpyAsync(&ngroups, gid + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     int32_t *gp0 = nullptr, *nsub = nullptr, *sub0 = nullptr;
-    int *d_stats = nullptr;     // [0] max width, [1] max record bytes
     if ((st = tmp.alloc_n(&gp0, (size_t)ngroups + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&nsub, (size_t)ngroups + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&sub0, (size_t)ngroups + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&d_stats, 4)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(int), s));
     const int gg = (ngroups + 1 + 255) / 256;
     k_group_start<<<eg, 256, 0, s>>>(head, gid, n, ngroups, gp0);
-    // rows per step: 32 (one per lane) unless the records would not leave room
-    // for >= kMinStages of them per warp in half the shared memory
-    const int maxw_all = std::min(h->info.max_row_deps, kTprMax);
-    int rc = 32;
-    while (rc > 4 && (size_t)kWPC * kMinStages * a16(rec_bytes(rc, maxw_all, (int)es)) > (size_t)max_smem / 2) rc /= 2;
-    B.rows_per_step = rc;
-    k_group_sub<<<gg, 256, 0, s>>>(gp0, ngroups, rc, nsub);
+    k_group_sub<<<gg, 256, 0, s>>>(gp0, ngroups, nsub);
     if ((st = exclusive_scan_i32(nsub, sub0, (int64_t)ngroups + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     int32_t nsteps = 0;
     SPTRSV_CUDA(cudaMemcpyAsync(&nsteps, sub0 + ngroups, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     B.nsteps = nsteps;
-    int4 *steps = nullptr;
-    int32_t *step_unit = nullptr, *step_of = nullptr;
-    int64_t *rb = nullptr;
+    int2 *steps = nullptr;
+    int32_t *step_unit = nullptr, *step_of = nullptr, *ppos = nullptr;
     if ((st = tmp.alloc_n(&steps, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&step_unit, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&step_of, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&rb, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&ppos, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc_n(&B.d_unit_step0, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_rec_off, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
-    k_steps<<<gg, 256, 0, s>>>(gp0, sub0, ngroups, rc, bperm, h->d_dp, unit, steps, step_unit, d_stats);
+    k_steps<<<gg, 256, 0, s>>>(gp0, sub0, ngroups, bperm, unit, steps, step_unit);
     k_unit_step0<<<(nsteps + 255) / 256, 256, 0, s>>>(step_unit, nsteps, U, B.d_unit_step0);
-    k_rec_sizes<<<(nsteps + 1 + 255) / 256, 256, 0, s>>>(steps, nsteps, (int)es, rb, d_stats + 1);
-    if ((st = exclusive_scan_i64(rb, B.d_rec_off, (int64_t)nsteps + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    k_pos_step<<<eg, 256, 0, s>>>(head, gid, gp0, sub0, n, rc, step_of);
+    k_pos_step<<<eg, 256, 0, s>>>(head, gid, gp0, sub0, steps, bperm, unit, B.d_unit_step0, n, step_of, ppos);
     SPTRSV_CUDA(cudaGetLastError());
-    int64_t rec_total = 0;
-    int hstats[4];
-    SPTRSV_CUDA(cudaMemcpyAsync(&rec_total, B.d_rec_off + nsteps, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    SPTRSV_CUDA(cudaMemcpyAsync(hstats, d_stats, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    std::vector<int32_t> hunit_rows((size_t)U);
-    SPTRSV_CUDA(cudaMemcpyAsync(hunit_rows.data(), unit_rows, sizeof(int32_t) * U, cudaMemcpyDeviceToHost, s));
-    // overflow CSR (entries beyond kTprMax), by position
-    int32_t *ocnt = nullptr;
-    if ((st = tmp.alloc_n(&ocnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_ovf_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, bperm, h->d_dp, ocnt);
-    if ((st = exclusive_scan_i32(ocnt, B.d_ovf_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    int32_t novf = 0;
-    SPTRSV_CUDA(cudaMemcpyAsync(&novf, B.d_ovf_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SPTRSV_CUDA(cudaStreamSynchronize(s));
-    const int maxw = hstats[0];
-    const int rec_max = (int)a16(hstats[1]);
-    B.maxw = maxw;
-    B.rec_max = rec_max;
-    B.nent = rec_total;
-    B.novf = novf;
-    int max_unit_rows = 0;
-    for (int v : hunit_rows) max_unit_rows = std::max(max_unit_rows, v);
-    B.max_unit_rows = max_unit_rows;
 
-    // ---- 4. shared memory: mbarriers | per-warp record rings | per-warp x slot rings
+    // ---- 4. record geometry, shared memory (mbarriers | record rings | x slots)
+    const int W = std::max(1, std::min(h->info.max_row_deps, kTprMax));
+    const int REC = rec_bytes(W, (int)es);
     int nst = 16;
-    while (nst > kMinStages && (size_t)kWPC * nst * rec_max > (size_t)max_smem / 2) nst /= 2;
-    const size_t fixed = 8 * (size_t)kWPC * nst + (size_t)kWPC * nst * rec_max;
-    if (fixed + (size_t)kWPC * (64 + (kBRing + kXRing * kTprMax) * 32) * es > (size_t)max_smem)
-        return SPTRSV_ERR_NOT_SUPPORTED;
-    const int maxw_t = maxw <= 4 ? 4 : (maxw <= 8 ? 8 : kTprMax);
-    const size_t rings = (size_t)kWPC * (kBRing * 32 + (size_t)kXRing * maxw_t * 32) * es;
-    int Wu = 1;
-    while ((size_t)kWPC * (2 * Wu + 1) * es + fixed + rings <= (size_t)max_smem) Wu *= 2;
+    while (nst > kMinStages && (size_t)kWPC * nst * REC > (size_t)max_smem / 2) nst /= 2;
+    const size_t fixed = 8 * (size_t)kWPC * nst + (size_t)kWPC * nst * REC;
+    if (fixed + (size_t)(kWPC * 64 + 1) * es > (size_t)max_smem) return SPTRSV_ERR_NOT_SUPPORTED;
+    int Wu = 32;
+    while ((size_t)(kWPC * 2 * Wu + 1) * es + fixed <= (size_t)max_smem) Wu *= 2;
     const int Wenv = env_int("SPTRSV_BLOCK_SLOTS", 0);
     if (Wenv > 0) {
-        int w2 = 1;
+        int w2 = 32;
         while (w2 * 2 <= Wenv) w2 *= 2;
         Wu = std::min(Wu, w2);
     }
+    const int Z = kWPC * Wu;
     B.W = Wu;
     B.nst = nst;
-    if ((st = h->arena.alloc(&B.d_recs, (size_t)std::max<int64_t>(rec_total, 16))) != SPTRSV_SUCCESS) return st;
+    B.maxw = W;
+    B.rec_max = REC;
+    B.nent = (int64_t)nsteps * REC;
+
+    // overflow CSR (entries beyond W), by position; row -> position
+    int32_t *ocnt = nullptr;
+    if ((st = tmp.alloc_n(&ocnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_ovf_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_ovf_pos, (size_t)n)) != SPTRSV_SUCCESS) return st;
+    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, bperm, h->d_dp, W, ocnt);
+    if ((st = exclusive_scan_i32(ocnt, B.d_ovf_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemcpyAsync(B.d_ovf_pos, pos, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    int32_t novf = 0;
+    SPTRSV_CUDA(cudaMemcpyAsync(&novf, B.d_ovf_ptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    B.novf = novf;
+
+    // ---- 5. records
+    if ((st = h->arena.alloc(&B.d_recs, (size_t)std::max<int64_t>((int64_t)nsteps * REC, 16))) != SPTRSV_SUCCESS)
+        return st;
     if ((st = h->arena.alloc_n(&B.d_ovf_col, (size_t)std::max(novf, 1))) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc(&B.d_ovf_val, (size_t)std::max(novf, 1) * es)) != SPTRSV_SUCCESS) return st;
-    if (h->dtype == SPTRSV_F64)
-        k_rec_fill<double><<<eg, 256, 0, s>>>(n, Wu, nst, unit, unit_rows, step_of, bperm, pos, steps, B.d_rec_off,
-                                             B.d_unit_step0, tri_ptr, tri_col, (const double *)tri_val,
-                                             (const double *)h->d_invd_row, B.d_ovf_ptr,
-                                             (unsigned char *)B.d_recs, B.d_ovf_col, (double *)B.d_ovf_val);
-    else
-        k_rec_fill<float><<<eg, 256, 0, s>>>(n, Wu, nst, unit, unit_rows, step_of, bperm, pos, steps, B.d_rec_off,
-                                            B.d_unit_step0, tri_ptr, tri_col, (const float *)tri_val,
-                                            (const float *)h->d_invd_row, B.d_ovf_ptr, (unsigned char *)B.d_recs,
-                                            B.d_ovf_col, (float *)B.d_ovf_val);
+    const int pg = (int)(((int64_t)nsteps * 32 + 255) / 256);
+    if (h->dtype == SPTRSV_F64) {
+        k_rec_pad<double><<<pg, 256, 0, s>>>(nsteps, W, Z, steps, (unsigned char *)B.d_recs);
+        k_rec_fill<double><<<eg, 256, 0, s>>>(n, Wu, W, Z, unit, B.d_unit_step0, step_of, bperm, ppos, steps, tri_ptr,
+                                             tri_col, (const double *)tri_val, (const double *)h->d_invd_row,
+                                             B.d_ovf_ptr, (unsigned char *)B.d_recs, B.d_ovf_col,
+                                             (double *)B.d_ovf_val);
+    } else {
+        k_rec_pad<float><<<pg, 256, 0, s>>>(nsteps, W, Z, steps, (unsigned char *)B.d_recs);
+        k_rec_fill<float><<<eg, 256, 0, s>>>(n, Wu, W, Z, unit, B.d_unit_step0, step_of, bperm, ppos, steps, tri_ptr,
+                                            tri_col, (const float *)tri_val, (const float *)h->d_invd_row,
+                                            B.d_ovf_ptr, (unsigned char *)B.d_recs, B.d_ovf_col,
+                                            (float *)B.d_ovf_val);
+    }
     SPTRSV_CUDA(cudaGetLastError());
 
     // ---- launch configuration: K co-resident CTAs of kWPC warps
-    const size_t smem = fixed + (size_t)kWPC * (Wu + 1) * es + rings;
+    const size_t smem = fixed + (size_t)(kWPC * Wu + 1) * es;
     void *kn = nullptr;
     for (int tr = 1; tr >= 0; --tr) {
         if (h->dtype == SPTRSV_F64)
-            kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(maxw, tr) : pick_kernel<double, false>(maxw, tr);
+            kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(W, tr) : pick_kernel<double, false>(W, tr);
         else
-            kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(maxw, tr) : pick_kernel<float, false>(maxw, tr);
+            kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(W, tr) : pick_kernel<float, false>(W, tr);
         SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (tr) B.kernel_trace = kn;
     }
@@ -819,11 +782,11 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     else
         k_bprefill<float><<<h->num_sms * 4, 512, 0, s>>>((float *)x, h->n);
     SPTRSV_CUDA(cudaGetLastError());
-    int Wu = B.W, nst = B.nst, rec_max = B.rec_max;
+    int Wu = B.W, W = B.maxw, nst = B.nst;
     const unsigned char *recs = (const unsigned char *)B.d_recs;
-    void *args[] = {(void *)&Wu, (void *)&nst, (void *)&rec_max, (void *)&B.d_unit_step0, (void *)&B.d_rec_off,
-                    (void *)&recs, (void *)&B.d_ovf_ptr, (void *)&B.d_ovf_col, (void *)&B.d_ovf_val, (void *)&b,
-                    (void *)&x};
+    void *args[] = {(void *)&Wu, (void *)&W, (void *)&nst, (void *)&B.d_unit_step0, (void *)&recs,
+                    (void *)&B.d_ovf_ptr, (void *)&B.d_ovf_col, (void *)&B.d_ovf_val, (void *)&B.d_ovf_pos,
+                    (void *)&b, (void *)&x};
     SPTRSV_CUDA(cudaLaunchCooperativeKernel(g_host_trace ? B.kernel_trace : B.kernel, B.nblocks, B.threads, args,
                                             B.smem, s));
     return SPTRSV_SUCCESS;

@@ -45,9 +45,9 @@ struct BlockPlan {
     void *kernel = nullptr;
     void *kernel_trace = nullptr;
     int32_t *d_unit_step0 = nullptr;  // [U+1]
-    int64_t *d_rec_off = nullptr;     // [nsteps+1] byte offsets of the step records
     void *d_recs = nullptr;           // step records (see block.cu)
     int32_t *d_ovf_ptr = nullptr;     // [n+1] by position
+    int32_t *d_ovf_pos = nullptr;     // [n] row -> position
     int32_t *d_ovf_col = nullptr;
     void *d_ovf_val = nullptr;
 };

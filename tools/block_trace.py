@@ -21,16 +21,16 @@ torch.cuda.synchronize()
 assert lib.sptrsv_dbg_block_trace(ctypes.c_void_p(buf.data_ptr()), cap) == 0
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda"); flush.zero_()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ph = torch.zeros(4 * 128, dtype=torch.int64, device="cuda")
+ph = torch.zeros(5 * 128, dtype=torch.int64, device="cuda")
 lib.sptrsv_dbg_block_phase(ctypes.c_void_p(ph.data_ptr()))
 ev0.record(); sv.solve(b); ev1.record(); torch.cuda.synchronize()
 lib.sptrsv_dbg_block_trace(None, 0)
 lib.sptrsv_dbg_block_phase(None)
-P = ph.view(128, 4).cpu().numpy().astype(np.int64)
+P = ph.view(128, 5).cpu().numpy().astype(np.int64)
 d = np.diff(P, axis=1)
-print("warp0 cycles (median steps 8..127): load_regs(s+2), prefetch_b, solve:", np.median(d[8:], axis=0).tolist(),
-      " loop gap:", float(np.median(P[9:, 0] - P[8:-1, 3])))
-print("warp0 per-step solve cycles steps 8..40:", d[8:40, 2].tolist())
+print("warp0 cycles (median steps 8..127): wait(s+2), lead, issue+prefetch_b, solve:",
+      np.median(d[8:], axis=0).tolist(), " loop gap:", float(np.median(P[9:, 0] - P[8:-1, 4])))
+
 
 t = buf.view(K, cap).cpu().numpy()
 t0 = t[t > 0].min()
