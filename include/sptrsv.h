@@ -56,7 +56,10 @@ typedef enum { SPTRSV_F64 = 0, SPTRSV_F32 = 1 } sptrsv_dtype_t;
 typedef enum {
     SPTRSV_ALGO_SELF = 0,   /* self-scheduled, per-row ready flags (SLFR) */
     SPTRSV_ALGO_LEVEL = 1,  /* level-scheduled, grid-wide barrier per level (LEVR) */
-    SPTRSV_ALGO_BLOCK = 2   /* self-scheduled over CTA-owned row blocks */
+    SPTRSV_ALGO_BLOCK = 2,  /* self-scheduled over warp-owned row tiles, register/shared-memory
+                               hand-offs (any matrix, fastest on structured grids) */
+    SPTRSV_ALGO_AUTO = 3    /* BLOCK when the analysis detects a structured grid, else SELF;
+                               info.algo then reports the algorithm chosen */
 } sptrsv_algo_t;
 
 typedef enum {
@@ -146,7 +149,10 @@ sptrsv_status_t sptrsv_solve_host(sptrsv_handle_t h, const void *b_host, void *x
 sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h);
 
 /* Selects the single-RHS algorithm (default SPTRSV_ALGO_SELF).  The BLOCK
- * schedule is built lazily on first use. */
+ * schedule is built lazily on first use (BLOCK or AUTO; device kernels on the
+ * default stream, synchronized).  Errors: INVALID_VALUE (NULL handle, bad
+ * enum), NOT_SUPPORTED (BLOCK only: the plan does not fit the device), the
+ * analysis status of a failed handle. */
 sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo);
 
 /* Copies the handle's summary into *info (host pointer). */

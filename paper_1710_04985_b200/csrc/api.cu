@@ -145,16 +145,19 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
 
 extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
     if (!h) return SPTRSV_ERR_INVALID_VALUE;
-    if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK)
+    if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK &&
+        algo != SPTRSV_ALGO_AUTO)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
-    if (algo == SPTRSV_ALGO_BLOCK && !h->block.built && h->n > 0) {
+    if ((algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_AUTO) && !h->block.built && h->n > 0) {
         SPTRSV_CUDA(cudaSetDevice(h->device));
         sptrsv_status_t st = block_build(h, nullptr);
-        if (st != SPTRSV_SUCCESS) return st;
-        h->info.nblocks = h->block.nblocks;
+        if (st != SPTRSV_SUCCESS && algo == SPTRSV_ALGO_BLOCK) return st;
+        h->info.nblocks = h->block.built ? h->block.nblocks : 0;
         h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
     }
+    if (algo == SPTRSV_ALGO_AUTO)
+        algo = (h->block.built && h->block.grid_nx > 0) ? SPTRSV_ALGO_BLOCK : SPTRSV_ALGO_SELF;
     h->algo = algo;
     h->info.algo = algo;
     return SPTRSV_SUCCESS;

@@ -34,22 +34,26 @@ struct DevArena {
 struct BlockPlan {
     bool built = false;
     int32_t nblocks = 0;      // K co-resident CTAs
-    int32_t nunits = 0;       // K x warps per CTA
-    int32_t W = 0;            // shared-memory x slots per warp (power of two)
-    int32_t nst = 0;          // TMA records in flight per warp
-    int32_t nsteps = 0;       // (unit, level) steps of <= 32 rows
-    int32_t maxw = 0, novf = 0, threads = 0, rec_max = 0, max_unit_rows = 0, rows_per_step = 32;
-    int32_t grid_nx = 0, grid_ny = 0, tiles_x = 0, tiles_y = 0;   // detected grid / tiles (0 = natural)
+    int32_t wpc = 0;          // warps per CTA
+    int32_t nunits = 0;       // K x wpc warps
+    int32_t W = 0;            // record entries per row (kernel instance)
+    int32_t nst = 0;          // record ring per warp (steps)
+    int32_t bb = 0;           // b lookahead (blocks)
+    int32_t nsteps = 0;       // (warp, level) steps of <= 32 rows
+    int32_t G = 0;            // global mailboxes (values read by another CTA)
+    int32_t nslots = 0;       // shared slots per CTA (values read by another warp of the CTA)
+    int32_t novf = 0, threads = 0, rec_bytes = 0;
+    int32_t grid_nx = 0, grid_ny = 0, tile_w = 0, tile_h = 0;   // detected grid / warp tile (0 = natural)
     int64_t nent = 0;         // record bytes
     size_t smem = 0;
     void *kernel = nullptr;
-    void *kernel_trace = nullptr;
-    int32_t *d_unit_step0 = nullptr;  // [U+1]
+    int32_t *d_unit_step0 = nullptr;  // [U+1] first step of every warp
     void *d_recs = nullptr;           // step records (see block.cu)
-    int32_t *d_ovf_ptr = nullptr;     // [n+1] by position
-    int32_t *d_ovf_pos = nullptr;     // [n] row -> position
-    int32_t *d_ovf_col = nullptr;
+    int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
+    int32_t *d_ovf_code = nullptr;    // overflow entries (rows with > W dependencies)
     void *d_ovf_val = nullptr;
+    void *d_gmb = nullptr;            // [2][G] mailboxes (value-as-flag), roles swap per solve
+    unsigned *d_ctr = nullptr;        // [0] solve epoch, [1] finished CTAs
 };
 
 }  // namespace sptrsv

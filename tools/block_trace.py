@@ -10,7 +10,7 @@ m, p = workloads.config(cfg)
 uplo, diag = ("lower", "unit") if cfg == 3 else (p["uplo"], p["diag"])
 sv = S.from_csr(m, uplo, diag, algo="block")
 info = sv.info()
-K = info["nblocks"] * 4
+K = info["nblocks"] * 8          # >= warps (wpc <= 8)
 cap = 4096
 buf = torch.zeros(K * cap, dtype=torch.int64, device="cuda")
 lib = ctypes.CDLL(S.LIB_PATH)
@@ -21,18 +21,20 @@ torch.cuda.synchronize()
 assert lib.sptrsv_dbg_block_trace(ctypes.c_void_p(buf.data_ptr()), cap) == 0
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda"); flush.zero_()
 ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-ph = torch.zeros(5 * 128, dtype=torch.int64, device="cuda")
+ph = torch.zeros(6 * 128, dtype=torch.int64, device="cuda")
 lib.sptrsv_dbg_block_phase(ctypes.c_void_p(ph.data_ptr()))
 ev0.record(); sv.solve(b); ev1.record(); torch.cuda.synchronize()
 lib.sptrsv_dbg_block_trace(None, 0)
 lib.sptrsv_dbg_block_phase(None)
-P = ph.view(128, 5).cpu().numpy().astype(np.int64)
+P = ph.view(128, 6).cpu().numpy().astype(np.int64)
 d = np.diff(P, axis=1)
-print("warp0 cycles (median steps 8..127): wait(s+2), lead, issue+prefetch_b, solve:",
-      np.median(d[8:], axis=0).tolist(), " loop gap:", float(np.median(P[9:, 0] - P[8:-1, 4])))
+print("warp0 cycles, median steps 8..120: cp.async wait | compute+stores+syncwarp | issue+wait(s+PB) | cp.async+wait(s+1) | load fields:",
+      np.median(d[8:120], axis=0).tolist(), " loop gap:", float(np.median(P[9:120, 0] - P[8:119, 5])))
 
 
 t = buf.view(K, cap).cpu().numpy()
+os.makedirs("gpurun_out", exist_ok=True)
+np.savez_compressed(f"gpurun_out/trace_cfg{cfg}.npz", t=t, info=json.dumps(info))
 t0 = t[t > 0].min()
 out = {"solve_us": ev0.elapsed_time(ev1) * 1e3, "K": K, "ctas": []}
 durs = []
@@ -42,9 +44,9 @@ for k in range(K):
     if len(nz) < 2:
         continue
     ts = row[nz] - t0
-    d = np.diff(ts)
+    d = np.diff(ts) / np.maximum(1, np.diff(nz))     # entries may be per block of steps
     durs.append(d)
-    out["ctas"].append({"cta": k, "start_us": ts[0] / 1e3, "end_us": ts[-1] / 1e3, "steps": len(nz) - 1,
+    out["ctas"].append({"warp": k, "start_us": ts[0] / 1e3, "end_us": ts[-1] / 1e3, "steps": int(nz[-1]),
                         "step_med_ns": float(np.median(d)), "step_p90_ns": float(np.percentile(d, 90))})
 alld = np.concatenate(durs)
 out["step_ns_median"] = float(np.median(alld)); out["step_ns_p90"] = float(np.percentile(alld, 90))
@@ -52,6 +54,6 @@ out["step_ns_mean"] = float(alld.mean())
 ends = [c["end_us"] for c in out["ctas"]]; starts = [c["start_us"] for c in out["ctas"]]
 out["first_start_us"] = min(starts); out["last_start_us"] = max(starts); out["last_end_us"] = max(ends)
 print(json.dumps({k: v for k, v in out.items() if k != "ctas"}))
-sel = sorted(out["ctas"], key=lambda c: c["cta"])
+sel = sorted(out["ctas"], key=lambda c: c["warp"])
 for c in sel[:: max(1, len(sel) // 12)]:
     print(json.dumps(c))
