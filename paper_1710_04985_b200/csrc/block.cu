@@ -54,9 +54,18 @@ __host__ __device__ inline int32_t code_glob(int g) { return (int32_t)((2u << 30
 __host__ __device__ inline unsigned code_kind(int32_t c) { return (unsigned)c >> 30; }
 __host__ __device__ inline int code_idx(int32_t c) { return c & 0x3FFFFFFF; }
 
-// record geometry (W entries per row; SoA over 32 lanes; both parts 16 B multiples)
-__host__ __device__ constexpr int rec_ibytes(int W) { return 32 * 4 * (4 + W); }
-__host__ __device__ constexpr int rec_bytes(int W, int es) { return rec_ibytes(W) + 32 * es * (1 + W); }
+// Record of one (warp, step), SoA over 32 lanes, every part a multiple of 16 B:
+//   compute part: int4 {row, oslot, og, srcs}[32]          (one LDS.128)
+//                 T {invd, a_0 .. a_SH-1}: (SH+1) values in 16-byte groups [g][32]
+//   helper part:  int ecode[WE][32] | T eval[WE][32]
+//   srcs: bits 0-2 = number of SHFL terms, then 5 bits per source lane.
+//   ecode[0] = kOvf | i: all EXT terms of the row are in the overflow list at i.
+__host__ __device__ constexpr int rec_cv(int) { return 512; }
+__host__ __device__ constexpr int rec_ec(int SH, int es) { return 512 + 32 * es * (SH + 1); }
+__host__ __device__ constexpr int rec_ev(int SH, int WE, int es) { return rec_ec(SH, es) + 128 * WE; }
+__host__ __device__ constexpr int rec_bytes(int SH, int WE, int es) { return rec_ev(SH, WE, es) + 32 * es * WE; }
+constexpr int kSH = 3;                       // SHFL terms per row (compute warp)
+constexpr int32_t kOvfTag = (int32_t)(3u << 30) | (1 << 29);     // kind NONE + bit 29: overflow index
 
 constexpr int kBuckets = kTprMax + 2;
 __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax ? 0u : (uint32_t)(kTprMax + 1 - deps); }
@@ -200,26 +209,34 @@ __global__ void k_cta_p0(int K, int wpc, int nsteps, int n, const int32_t *unit_
     cta_p0[c] = s < nsteps ? steps[s].x : n;
 }
 
-// Dependency classes -> which producers need a shared slot (bit 0) or a global
-// mailbox (bit 1).  A row with more than W dependencies (or in a CTA whose
-// slots overflowed: noslot) takes no SHFL / SMEM codes respectively.
-__global__ void k_need(int n, int W, int wpc, const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
-                       const int32_t *__restrict__ unit, const int32_t *__restrict__ pos,
-                       const int32_t *__restrict__ step_of, const unsigned char *__restrict__ noslot,
-                       int32_t *need) {
+// Dependency classes.  Walking a row's dependencies in storage order, the
+// first SH that were solved by the same warp in the previous step are SHFL
+// (the compute warp's registers); the others are EXT, resolved by the helper
+// warp: from a shared slot (producer in the same CTA, bit 0 of need) or from
+// a global mailbox (bit 1).  noslot: that CTA's slots overflowed -> GLOB.
+// ecnt[pos] = number of EXT dependencies of the row at solve position pos.
+__global__ void k_need(int n, int SH, int wpc, const int32_t *__restrict__ tri_ptr,
+                       const int32_t *__restrict__ tri_col, const int32_t *__restrict__ unit,
+                       const int32_t *__restrict__ pos, const int32_t *__restrict__ step_of,
+                       const unsigned char *__restrict__ noslot, int32_t *need, int32_t *ecnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int a = tri_ptr[i], e = tri_ptr[i + 1];
-    const bool ovf = e - a > W;
     const int ui = unit[i], si = step_of[pos[i]];
     const bool ns = noslot[ui / wpc] != 0;
+    int nsh = 0, next = 0;
     for (int k = a; k < e; ++k) {
         const int j = tri_col[k];
         const int uj = unit[j], pj = pos[j];
-        if (!ovf && uj == ui && step_of[pj] == si - 1) continue;        // SHFL
+        if (nsh < SH && uj == ui && step_of[pj] == si - 1) {
+            ++nsh;
+            continue;
+        }
+        ++next;
         if (uj / wpc == ui / wpc && !ns) atomicOr(&need[pj], 1);
         else atomicOr(&need[pj], 2);
     }
+    ecnt[pos[i]] = next;
 }
 
 __global__ void k_need_bits(int n, const int32_t *need, int bit, int32_t *out) {
@@ -228,13 +245,9 @@ __global__ void k_need_bits(int n, const int32_t *need, int bit, int32_t *out) {
     if (p == n) out[p] = 0;
 }
 
-__global__ void k_ovf_count(int n, int W, const int32_t *bperm, const int32_t *tri_ptr, int32_t *cnt) {
+__global__ void k_ovf_count(int n, int WE, const int32_t *ecnt, int32_t *cnt) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) {
-        const int i = bperm[p];
-        const int d = tri_ptr[i + 1] - tri_ptr[i];
-        cnt[p] = d > W ? d + 1 : 0;          // + terminator
-    }
+    if (p < n) cnt[p] = ecnt[p] > WE ? ecnt[p] + 1 : 0;       // + terminator
     if (p == n) cnt[p] = 0;
 }
 
@@ -246,89 +259,76 @@ __global__ void k_cta_slots(int K, const int32_t *cta_p0, const int32_t *slot_sc
 
 // one thread per (step, lane): the record of that lane (padding lanes included)
 template <typename T>
-__global__ void k_rec_fill(int nsteps, int W, int wpc, const int2 *__restrict__ steps,
-                           const int32_t *__restrict__ step_unit, const int32_t *__restrict__ bperm,
-                           const int32_t *__restrict__ pos, const int32_t *__restrict__ step_of,
-                           const int32_t *__restrict__ unit, const int32_t *__restrict__ tri_ptr,
-                           const int32_t *__restrict__ tri_col, const T *__restrict__ tri_val,
-                           const T *__restrict__ invd_row, const unsigned char *__restrict__ noslot,
-                           const int32_t *__restrict__ need, const int32_t *__restrict__ slot_scan,
+__global__ void k_rec_fill(int nsteps, int SH, int WE, int wpc, const int2 *__restrict__ steps,
+                           const int32_t *__restrict__ bperm, const int32_t *__restrict__ pos,
+                           const int32_t *__restrict__ step_of, const int32_t *__restrict__ unit,
+                           const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
+                           const T *__restrict__ tri_val, const T *__restrict__ invd_row, int unit_diag,
+                           const unsigned char *__restrict__ noslot, const int32_t *__restrict__ need,
+                           const int32_t *__restrict__ ecnt, const int32_t *__restrict__ slot_scan,
                            const int32_t *__restrict__ g_scan, const int32_t *__restrict__ cta_p0,
                            const int32_t *__restrict__ ovf_ptr, unsigned char *__restrict__ recs,
-                           int32_t *__restrict__ ovf_code, T *__restrict__ ovf_val) {
+                           int32_t *__restrict__ rows, int32_t *__restrict__ ovf_code, T *__restrict__ ovf_val) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)nsteps * 32) return;
     const int s = (int)(t >> 5), lane = (int)(t & 31);
-    const int REC = rec_bytes(W, sizeof(T));
-    unsigned char *base = recs + (size_t)s * REC;
-    int32_t *ip = reinterpret_cast<int32_t *>(base);
-    T *vp = reinterpret_cast<T *>(base + rec_ibytes(W));
+    const int es = (int)sizeof(T), G16 = 16 / es;
+    rows[t] = lane < steps[s].y ? bperm[steps[s].x + lane] : -1;            // values per 16-byte group
+    unsigned char *base = recs + (size_t)s * rec_bytes(SH, WE, es);
+    int4 *ci = reinterpret_cast<int4 *>(base);
+    T *cv = reinterpret_cast<T *>(base + rec_cv(SH));
+    int32_t *ec = reinterpret_cast<int32_t *>(base + rec_ec(SH, es));
+    T *ev = reinterpret_cast<T *>(base + rec_ev(SH, WE, es));
+    auto cvp = [&](int q) -> T & { return cv[((q / G16) * 32 + lane) * G16 + (q % G16)]; };
     const int2 st = steps[s];
+    for (int q = 0; q <= SH; ++q) cvp(q) = T(0);
+    for (int q = 0; q < WE; ++q) {
+        ec[q * 32 + lane] = kNone;
+        ev[q * 32 + lane] = T(0);
+    }
     if (lane >= st.y) {
-        ip[lane] = -1;
-        ip[32 + lane] = -1;
-        ip[64 + lane] = -1;
-        ip[96 + lane] = -1;
-        for (int k = 0; k < W; ++k) {
-            ip[(4 + k) * 32 + lane] = kNone;
-            vp[(1 + k) * 32 + lane] = T(0);
-        }
-        vp[lane] = T(0);
+        ci[lane] = make_int4(-1, -1, -1, 0);
         return;
     }
     const int p = st.x + lane;
     const int i = bperm[p];
-    const int ui = unit[i], ci = ui / wpc;
-    const bool ns = noslot[ci] != 0;
+    const int ui = unit[i], cta = ui / wpc;
+    const bool ns = noslot[cta] != 0;
     const int nd = need[p];
-    ip[lane] = i;
-    ip[32 + lane] = (nd & 1) ? slot_scan[p] - slot_scan[cta_p0[ci]] : -1;
-    ip[64 + lane] = (nd & 2) ? g_scan[p] : -1;
-    vp[lane] = invd_row[i];
+    const int si = step_of[p];
     const int a = tri_ptr[i], e = tri_ptr[i + 1];
-    const bool ovf = e - a > W;
-    auto code_of = [&](int j, bool allow_shfl, bool &is_shfl) -> int32_t {
+    const bool ovf = ecnt[p] > WE;
+    int srcs = 0, nsh = 0, ne = 0;
+    int o = ovf ? ovf_ptr[p] : 0;
+    if (ovf) ec[lane] = kOvfTag | o;
+    for (int k = a; k < e; ++k) {
+        const int j = tri_col[k];
         const int uj = unit[j], pj = pos[j];
-        is_shfl = false;
-        if (allow_shfl && uj == ui && step_of[pj] == s - 1) {
-            is_shfl = true;
-            return pj - steps[s - 1].x;                       // lane of j in the previous step
+        if (nsh < SH && uj == ui && step_of[pj] == si - 1) {
+            srcs |= (pj - steps[si - 1].x) << (3 + 5 * nsh);
+            cvp(1 + nsh) = tri_val[k];
+            ++nsh;
+            continue;
         }
-        if (uj / wpc == ci && !ns) return code_smem(slot_scan[pj] - slot_scan[cta_p0[ci]]);
-        return code_glob(g_scan[pj]);
-    };
-    if (ovf) {
-        ip[96 + lane] = ovf_ptr[p];
-        int o = ovf_ptr[p];
-        bool sh;
-        for (int k = a; k < e; ++k, ++o) {
-            ovf_code[o] = code_of(tri_col[k], false, sh);
+        const int32_t c = (uj / wpc == cta && !ns) ? code_smem(slot_scan[pj] - slot_scan[cta_p0[cta]])
+                                                   : code_glob(g_scan[pj]);
+        if (ovf) {
+            ovf_code[o] = c;
             ovf_val[o] = tri_val[k];
+            ++o;
+        } else {
+            ec[ne * 32 + lane] = c;
+            ev[ne * 32 + lane] = tri_val[k];
+            ++ne;
         }
+    }
+    if (ovf) {
         ovf_code[o] = kNone;
         ovf_val[o] = T(0);
-        for (int k = 0; k < W; ++k) {
-            ip[(4 + k) * 32 + lane] = kNone;
-            vp[(1 + k) * 32 + lane] = T(0);
-        }
-        return;
     }
-    ip[96 + lane] = -1;
-    // non-SHFL terms first, then SHFL terms, each in storage order
-    int w = 0;
-    for (int pass = 0; pass < 2; ++pass)
-        for (int k = a; k < e; ++k) {
-            bool sh;
-            const int32_t c = code_of(tri_col[k], true, sh);
-            if (sh != (pass == 1)) continue;
-            ip[(4 + w) * 32 + lane] = c;
-            vp[(1 + w) * 32 + lane] = tri_val[k];
-            ++w;
-        }
-    for (; w < W; ++w) {
-        ip[(4 + w) * 32 + lane] = kNone;
-        vp[(1 + w) * 32 + lane] = T(0);
-    }
+    cvp(0) = unit_diag ? T(1) : invd_row[i];
+    ci[lane] = make_int4(i, (nd & 1) ? slot_scan[p] - slot_scan[cta_p0[cta]] : -1, (nd & 2) ? g_scan[p] : -1,
+                         srcs | nsh);
 }
 
 template <typename T>
@@ -409,6 +409,7 @@ __device__ unsigned long long *g_phase = nullptr;   // warp 0: 6 clock64 stamps 
 struct BlockArgs {
     const int32_t *unit_step0;
     const unsigned char *recs;
+    const int32_t *rows;          // [nsteps][32] row of every lane (-1: padding)
     const int32_t *cta_g0;
     const int32_t *ovf_code;
     const void *ovf_val;
@@ -416,16 +417,7 @@ struct BlockArgs {
     unsigned *ctr;
     const void *b;
     void *x;
-    int G, nst, nslots, bb;
-};
-
-template <typename T, int W>
-struct Fields {
-    int row, oslot, og, ovf;
-    int32_t code[W];
-    T invd;
-    T val[W];
-    T g[W];
+    int G, nslots;
 };
 
 // predicated value-as-flag loads (no branch: returns 0 where !pred)
@@ -453,12 +445,18 @@ __device__ __forceinline__ float lds_flag_if(const float *p, bool pred) {
                  : "+r"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
     return __uint_as_float(v);
 }
-
 __device__ __forceinline__ void sts_flag(double *p, double v) {
     asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v));
 }
 __device__ __forceinline__ void sts_flag(float *p, float v) {
     asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
+}
+// store ordered after every earlier memory access of the thread (compiler side)
+__device__ __forceinline__ void sts_flag_last(double *p, double v) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_flag_last(float *p, float v) {
+    asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
 }
 __device__ __forceinline__ void stg_flag(double *p, double v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v)));
@@ -466,17 +464,6 @@ __device__ __forceinline__ void stg_flag(double *p, double v) {
 __device__ __forceinline__ void stg_flag(float *p, float v) {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(__float_as_uint(v)));
 }
-
-// Pipeline per warp, in blocks of UB steps (no mbarrier on the step path;
-// cp.async groups are per thread, one group per block):
-//   group G(k), issued at the end of block k = { records of block k + NB
-//   (every lane copies 16-byte pieces), b[row] of block k + BB (own lane) },
-//   ring = NB blocks of records, BB blocks of b, NB >= 2 BB.
-//   Start of block k: cp.async.wait_group(BB - 1) + __syncwarp -> every group
-//   <= G(k - BB) landed in every lane: b of block k, the records of block k
-//   and of block k + BB (whose rows the b gather of G(k) needs).
-//   Then the UB records and b values go to registers (LDS), and the UB steps
-//   run back to back: only shuffles, FMAs and stores between two levels.
 __device__ __forceinline__ void cp_async_wait_n(int n) {      // n <= 7
     switch (n) {
         case 0: cp_async_wait<0>(); break;
@@ -490,23 +477,99 @@ __device__ __forceinline__ void cp_async_wait_n(int n) {      // n <= 7
     }
 }
 
-template <typename T, bool UNIT, int W, int UB>
+// the SH + 1 record values {invd, a_0 .. a_SH-1} of one lane (16-byte groups)
+template <typename T> struct CV;
+template <> struct CV<double> {
+    double v[4];
+    __device__ __forceinline__ void load(const unsigned char *p, int lane) {
+        const double2 g0 = reinterpret_cast<const double2 *>(p)[lane];
+        const double2 g1 = reinterpret_cast<const double2 *>(p + 512)[lane];
+        v[0] = g0.x; v[1] = g0.y; v[2] = g1.x; v[3] = g1.y;
+    }
+};
+template <> struct CV<float> {
+    float v[4];
+    __device__ __forceinline__ void load(const unsigned char *p, int lane) {
+        const float4 g0 = reinterpret_cast<const float4 *>(p)[lane];
+        v[0] = g0.x; v[1] = g0.y; v[2] = g0.z; v[3] = g0.w;
+    }
+};
+static_assert(kSH == 3, "CV<T> holds invd + 3 SHFL coefficients");
+
+// predicated cp.async of one value (no branch; nothing copied where !pred)
+__device__ __forceinline__ void cp_async_val_if(double *dst, const double *src, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 8;\n\t}" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"((unsigned)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_val_if(float *dst, const float *src, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"((unsigned)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_wd(uint64_t *bar, uint32_t ph) {
+    if (!mbar_try_wait(bar, ph)) {
+        const unsigned long long t0 = wd_now();
+        while (!mbar_try_wait(bar, ph))
+            if (wd_expired(t0)) break;
+    }
+}
+
+// Warp-specialised tile solve.  A CTA owns ntw tiles; tile w has a COMPUTE
+// warp (warp w) and a HELPER warp (warp ntw + w).  The helper works in blocks
+// of UB steps:
+//   records   block k+DB by one TMA bulk copy (ring of NBB blocks, mbarrier per slot)
+//   row ids   block k+R1B by one TMA bulk copy (ring of RRB blocks)
+//   b[row]    block k+R2B by cp.async, one group per block
+//   EXT terms of the block's UB steps: all their loads issued first (shared
+//             slots / global mailboxes, value-as-flag), then per step
+//             c = b - sum_EXT a x (storage order) -> the step's c slot
+//             (value-as-flag: the NaN sentinel while empty)
+// The compute warp, per step: waits for its lane's c, x = (c - sum_SHFL a
+// x_prev) * invd with the SHFL sources shuffled from the previous step's
+// results, stores x (and the shared slot / mailbox copies other warps need)
+// and re-arms the c slot.  Its critical chain between two levels is shuffle
+// -> FMA chain -> multiply.  The helper runs at most (NBB - DB) blocks ahead:
+// record slot k+DB reuses the slot of block k+DB-NBB, free once the compute
+// warp re-armed the c slot of that block's last step.
+constexpr int kDB = 3, kNBB = 5, kR2B = 2, kBR = kR2B + 1, kR1B = 4, kRRB = 4, kPFB = 12;
+__host__ __device__ constexpr int ub_of(int WE) { return WE <= 4 ? 4 : 2; }   // steps per helper block
+template <typename T, bool UNIT, int WE>
 __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
-    constexpr int REC = rec_bytes(W, sizeof(T));
-    constexpr int IB = rec_ibytes(W);
-    constexpr int NPIECE = REC * UB / 16;         // 16-byte pieces of one block of records
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-    const int nst = a.nst;                        // ring length in steps (NB * UB)
-    const int NB = nst / UB, BB = a.bb;
-    unsigned char *rings = smem_raw;
-    T *bring = reinterpret_cast<T *>(smem_raw + (size_t)wpc * nst * REC);
-    T *slots = bring + wpc * BB * UB * 32;
+    constexpr int SH = kSH, UB = ub_of(WE), DB = kDB, NBB = kNBB, R2B = kR2B, R1B = kR1B, RRB = kRRB;
+    constexpr int ES = (int)sizeof(T);
+    constexpr int REC = rec_bytes(SH, WE, ES);
+    constexpr int CVO = rec_cv(SH), ECO = rec_ec(SH, ES), EVO = rec_ev(SH, WE, ES);
+    constexpr int NCS = NBB * UB;                 // c ring (steps)
+    constexpr size_t TILE = ((size_t)NBB * UB * REC + (size_t)RRB * UB * 128 + (size_t)NCS * 32 * ES +
+                             (size_t)kBR * UB * 32 * ES + 8 * (NBB + RRB) + 127) / 128 * 128;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ntw = blockDim.x >> 6;
+    const int w = warp % ntw;
+    const bool helper = warp >= ntw;
+    unsigned char *tb = smem_raw + (size_t)w * TILE;
+    unsigned char *ring = tb;                                        // [NBB*UB][REC]
+    int32_t *rw = reinterpret_cast<int32_t *>(tb + (size_t)NBB * UB * REC);      // [RRB*UB][32]
+    T *cr = reinterpret_cast<T *>(rw + RRB * UB * 32);              // [NCS][32]
+    T *br = cr + NCS * 32;                                           // [kBR*UB][32]
+    uint64_t *recbar = reinterpret_cast<uint64_t *>(br + kBR * UB * 32);
+    uint64_t *rowbar = recbar + NBB;
+    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)ntw * TILE);
     const T *b = static_cast<const T *>(a.b);
     T *x = static_cast<T *>(a.x);
 
     for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
+    if (helper) {
+        for (int i = lane; i < NCS * 32; i += 32) cr[i] = Sentinel<T>::value();
+        if (lane == 0) {
+            for (int i = 0; i < NBB + RRB; ++i) mbar_init(&recbar[i], 1);
+            fence_mbar_init();
+        }
+    }
     if (threadIdx.x == 0) s_epoch = (unsigned)ld_relaxed(reinterpret_cast<const int *>(a.ctr));
     __syncthreads();
     const unsigned par = s_epoch & 1u;
@@ -517,142 +580,275 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
             go[i] = Sentinel<T>::value();
     }
 
-    const int u = blockIdx.x * wpc + warp;
-    const int s0 = a.unit_step0[u], s1 = a.unit_step0[u + 1];
-    if (s0 < s1) {
-        unsigned char *ring = rings + (size_t)warp * nst * REC;
-        T *br = bring + warp * BB * UB * 32;
-        const int nblk = (s1 - s0 + UB - 1) / UB;
-        // a warp's last block may read past its steps (the next warp's records,
-        // or the analysis' padding steps): they are never solved
-        auto blk_of = [&](int k) { return ring + (size_t)(k % NB) * (UB * REC); };
-        auto issue_rec = [&](int k) {            // block k of this warp
-            const unsigned char *src = a.recs + (size_t)(s0 + k * UB) * REC;
-            unsigned char *dst = blk_of(k);
-#pragma unroll
-            for (int q = lane; q < NPIECE; q += 32) cp_async_16(dst + 16 * q, src + 16 * q);
+    const int u = blockIdx.x * ntw + w;
+    const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;
+    if (n > 0 && helper) {
+        const int nblk = (n + UB - 1) / UB;
+        const unsigned char *grec = a.recs + (size_t)s0 * REC;
+        const int32_t *grow = a.rows + (size_t)s0 * 32;
+        const bool trace = g_trace != nullptr;
+        // lane 0: TMA of record block kk into ring block slot, row-id block kk into its slot
+        auto issue_rec = [&](int kk, int slot) {
+            mbar_arrive_expect_tx(&recbar[slot], UB * REC);
+            bulk_g2s(ring + (size_t)slot * UB * REC, grec + (size_t)kk * UB * REC, UB * REC, &recbar[slot]);
         };
-        auto issue_b = [&](int k) {
+        auto issue_rows = [&](int kk, int slot) {
+            mbar_arrive_expect_tx(&rowbar[slot], UB * 128);
+            bulk_g2s(rw + slot * UB * 32, grow + (size_t)kk * UB * 32, UB * 128, &rowbar[slot]);
+        };
+        auto prefetch_l2 = [&](int kk) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grec + (size_t)kk * UB * REC), "r"(UB * REC)
+                         : "memory");
+        };
+        auto issue_b = [&](int rslot, int bslot) {       // b of one block, rows from row-ring slot rslot
+            const int32_t *rr = rw + rslot * UB * 32 + lane;
+            T *bb = br + bslot * UB * 32 + lane;
 #pragma unroll
             for (int j = 0; j < UB; ++j) {
-                const int r = reinterpret_cast<const int32_t *>(blk_of(k) + j * REC)[lane];
-                if (r >= 0) cp_async_val(&br[(((k % BB) * UB) + j) * 32 + lane], b + r);
+                const int r = rr[j * 32];
+                cp_async_val_if(bb + j * 32, b + r, r >= 0);
             }
         };
-        // SMEM values: loaded one step ahead (shared-memory latency);
-        // GLOB values (another SM, an L2 round trip): one whole block ahead
-        auto prefetch_smem = [&](Fields<T, W> &F) {
-#pragma unroll
-            for (int q = 0; q < W; ++q)
-                if (code_kind(F.code[q]) != 2u)
-                    F.g[q] = lds_flag_if(slots + code_idx(F.code[q]), code_kind(F.code[q]) == 1u);
-        };
-        auto prefetch_glob = [&](T (&g)[UB][W], int k) {
+        // EXT values of one block: loaded one block ahead (an L2 round trip of slack)
+        int32_t ncode[UB][WE];
+        T nv[UB][WE];
+        auto ext_loads = [&](const unsigned char *rb, int kk) {
 #pragma unroll
             for (int j = 0; j < UB; ++j) {
-                const int32_t *ip = reinterpret_cast<const int32_t *>(blk_of(k) + j * REC);
+                const int32_t *ec = reinterpret_cast<const int32_t *>(rb + j * REC + ECO) + lane;
+                const bool vj = kk * UB + j < n;          // the last block may hold the next warp's steps
 #pragma unroll
-                for (int q = 0; q < W; ++q) {
-                    const int32_t c = ip[(4 + q) * 32 + lane];
-                    g[j][q] = ldg_flag_if(gm + code_idx(c), code_kind(c) == 2u);
+                for (int q = 0; q < WE; ++q) {
+                    ncode[j][q] = ec[q * 32];
+                    const unsigned kind = code_kind(ncode[j][q]);
+                    const T vs_ = lds_flag_if(slots + code_idx(ncode[j][q]), vj && kind == 1u);
+                    const T vg_ = ldg_flag_if(gm + code_idx(ncode[j][q]), vj && kind == 2u);
+                    nv[j][q] = kind == 1u ? vs_ : vg_;
                 }
             }
         };
-
+        if (lane == 0) {
+            for (int kk = 0; kk < min(nblk, kPFB); ++kk) prefetch_l2(kk);
+            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk, kk);
+            for (int kk = 0; kk < min(nblk, R1B); ++kk) issue_rows(kk, kk);
+        }
+        // b of blocks 0 .. R2B-1 (one cp.async group each)
 #pragma unroll 1
-        for (int k = 0; k < min(nblk, NB); ++k) issue_rec(k);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncwarp();
-#pragma unroll 1
-        for (int k = 0; k < BB; ++k) {
-            if (k < nblk) issue_b(k);
+        for (int kk = 0; kk < R2B; ++kk) {
+            if (kk < nblk) {
+                mbar_wait_wd(&rowbar[kk], 0u);
+                issue_b(kk, kk);
+            }
             cp_async_commit();
         }
-        T gnx[UB][W];
-        prefetch_glob(gnx, 0);
-        T xprev = T(0);
-        const bool trace = g_trace != nullptr;
+        mbar_wait_wd(&recbar[0], 0u);
+        __syncwarp();
+        ext_loads(ring, 0);
+        // ring positions (blocks) and mbarrier phases, kept incrementally
+        int rs = 0, rsph = 0;                 // record slot of block k, its phase
+        int rd = DB % NBB;                    // record slot of block k+DB
+        int ro = R1B % RRB;                   // row slot of block k+R1B
+        int rq = R2B % RRB, rqph = (R2B / RRB) & 1;   // row slot / phase of block k+R2B
+        int bs = 0, bw = R2B % kBR;           // b block slot of block k / of block k+R2B
+        int cs = 0;                           // c slot (steps) of the block's first step
+        int cf = (DB * UB + UB - 1) % NCS;    // c slot of the last step of block k+DB-NBB
 #pragma unroll 1
         for (int k = 0; k < nblk; ++k) {
             if (trace && lane == 0 && k * UB < g_trace_cap - 1) g_trace[(size_t)u * g_trace_cap + k * UB] = wd_now();
-            cp_async_wait_n(BB - 1);
-            __syncwarp();
-            Fields<T, W> F[UB];
-            T bv[UB];
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const unsigned char *r = blk_of(k) + j * REC;
-                const int32_t *ip = reinterpret_cast<const int32_t *>(r);
-                const T *vp = reinterpret_cast<const T *>(r + IB);
-                F[j].row = ip[lane];
-                F[j].oslot = ip[32 + lane];
-                F[j].og = ip[64 + lane];
-                F[j].ovf = ip[96 + lane];
-#pragma unroll
-                for (int q = 0; q < W; ++q) F[j].code[q] = ip[(4 + q) * 32 + lane];
-                F[j].invd = vp[lane];
-#pragma unroll
-                for (int q = 0; q < W; ++q) F[j].val[q] = vp[(1 + q) * 32 + lane];
-                bv[j] = br[(((k % BB) * UB) + j) * 32 + lane];
-#pragma unroll
-                for (int q = 0; q < W; ++q) F[j].g[q] = gnx[j][q];
-            }
-            if (k + 1 < nblk) prefetch_glob(gnx, k + 1);
-            prefetch_smem(F[0]);
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                if (UB > 1 && k * UB + j >= s1 - s0) break;          // warp-uniform tail
-                // SHFL sources from the previous step's registers; SMEM / GLOB
-                // values were prefetched (re-polled only if still the sentinel)
-                T vs[W];
-#pragma unroll
-                for (int q = 0; q < W; ++q) vs[q] = __shfl_sync(0xffffffffu, xprev, F[j].code[q] & 31);
-                bool pend = false;
-#pragma unroll
-                for (int q = 0; q < W; ++q) pend |= Sentinel<T>::is(F[j].g[q]);
-                if (pend) {
-#pragma unroll
-                    for (int q = 0; q < W; ++q)
-                        if (Sentinel<T>::is(F[j].g[q]))
-                            F[j].g[q] = code_kind(F[j].code[q]) == 1u ? poll_smem_slow(slots + code_idx(F[j].code[q]))
-                                                                     : poll_global_slow(gm + code_idx(F[j].code[q]));
-                }
-                T acc = bv[j];
-#pragma unroll
-                for (int q = 0; q < W; ++q)
-                    acc = fnma(F[j].val[q], code_kind(F[j].code[q]) == 0u ? vs[q] : F[j].g[q], acc);
-                if (F[j].ovf >= 0) {
-                    const T *ov = static_cast<const T *>(a.ovf_val);
-                    for (int o = F[j].ovf;; ++o) {
-                        const int32_t c = a.ovf_code[o];
-                        if (c == kNone) break;
-                        T v;
-                        if (code_kind(c) == 1u) {
-                            v = lds_volatile(slots + code_idx(c));
-                            if (Sentinel<T>::is(v)) v = poll_smem_slow(slots + code_idx(c));
-                        } else {
-                            v = ld_relaxed_val(gm + code_idx(c));
-                            if (Sentinel<T>::is(v)) v = poll_global_slow(gm + code_idx(c));
+            // (1) refill: records k+DB (its slot must be released by the compute warp), rows k+R1B
+            if (k + DB < nblk) {
+                if (k + DB >= NBB) {
+                    const T *f = cr + cf * 32 + lane;
+                    if (__any_sync(0xffffffffu, !Sentinel<T>::is(lds_volatile(f)))) {
+                        const unsigned long long t0 = wd_now();
+                        unsigned it = 0;
+                        while (__any_sync(0xffffffffu, !Sentinel<T>::is(lds_volatile(f)))) {
+                            __nanosleep(20);
+                            if ((++it & 1023u) == 0 && wd_expired(t0)) break;
                         }
-                        acc = fnma(ov[o], v, acc);
                     }
                 }
-                const T xi = Sentinel<T>::scrub(UNIT ? acc : acc * F[j].invd);
-                if (F[j].oslot >= 0) sts_flag(slots + F[j].oslot, xi);
-                if (F[j].og >= 0) stg_flag(gm + F[j].og, xi);
-                if (F[j].row >= 0) __stcg(x + F[j].row, xi);
-                xprev = xi;
-                if (j + 1 < UB) prefetch_smem(F[j + 1]);
+                if (lane == 0) issue_rec(k + DB, rd);
             }
-            __syncwarp();                       // every lane is done with block k: its ring slots are free
-            if (k + NB < nblk) issue_rec(k + NB);
-            if (k + BB < nblk) issue_b(k + BB);
+            if (lane == 0) {
+                if (k + R1B < nblk) issue_rows(k + R1B, ro);
+                if (k + kPFB < nblk) prefetch_l2(k + kPFB);
+            }
+            // (2) b of block k+R2B (row ids landed: mbarrier)
+            if (k + R2B < nblk) {
+                mbar_wait_wd(&rowbar[rq], (uint32_t)rqph);
+                issue_b(rq, bw);
+            }
             cp_async_commit();
+            // (3) block k: records (mbarrier) and b (cp.async group k)
+            cp_async_wait<R2B>();
+            mbar_wait_wd(&recbar[rs], (uint32_t)rsph);
+            __syncwarp();
+            const unsigned char *rb = ring + (size_t)rs * UB * REC;
+            int32_t code[UB][WE];
+            T v[UB][WE];
+#pragma unroll
+            for (int j = 0; j < UB; ++j)
+#pragma unroll
+                for (int q = 0; q < WE; ++q) {
+                    code[j][q] = ncode[j][q];
+                    v[j][q] = nv[j][q];
+                }
+            // (4) EXT loads of block k+1
+            if (k + 1 < nblk) {
+                const int rs1 = rs + 1 == NBB ? 0 : rs + 1;
+                mbar_wait_wd(&recbar[rs1], (uint32_t)(rs1 == 0 ? rsph ^ 1 : rsph));
+                ext_loads(ring + (size_t)rs1 * UB * REC, k + 1);
+            }
+            // (5) block k's c values.  Fast path (every EXT value arrived, no
+            // overflow row): straight-line over the UB steps.  Otherwise one step
+            // at a time, publishing each c as soon as its values are there (a
+            // later step of the block may depend on this warp's own results),
+            // re-issuing all pending loads of the block together per round trip.
+            bool pend = false, ovf = false;
+#pragma unroll
+            for (int j = 0; j < UB; ++j) {
+#pragma unroll
+                for (int q = 0; q < WE; ++q) pend |= Sentinel<T>::is(v[j][q]);
+                ovf |= ((unsigned)code[j][0] & 0xE0000000u) == 0xE0000000u && k * UB + j < n;
+            }
+            const T *evb = reinterpret_cast<const T *>(rb + EVO) + lane;
+            if (!__any_sync(0xffffffffu, pend || ovf)) {
+#pragma unroll
+                for (int j = 0; j < UB; ++j) {
+                    T c = br[(bs * UB + j) * 32 + lane];
+#pragma unroll
+                    for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
+                    sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < UB; ++j) {
+                    if (k * UB + j >= n) break;
+                    bool pj = false;
+#pragma unroll
+                    for (int q = 0; q < WE; ++q) pj |= Sentinel<T>::is(v[j][q]);
+                    if (__any_sync(0xffffffffu, pj)) {
+                        const unsigned long long t0 = wd_now();
+                        unsigned it = 0;
+                        do {
+#pragma unroll
+                            for (int jj = j; jj < UB; ++jj)
+#pragma unroll
+                                for (int q = 0; q < WE; ++q) {
+                                    const bool p = Sentinel<T>::is(v[jj][q]);
+                                    const unsigned kind = code_kind(code[jj][q]);
+                                    const T vs_ = lds_flag_if(slots + code_idx(code[jj][q]), p && kind == 1u);
+                                    const T vg_ = ldg_flag_if(gm + code_idx(code[jj][q]), p && kind == 2u);
+                                    v[jj][q] = p ? (kind == 1u ? vs_ : vg_) : v[jj][q];
+                                }
+                            pj = false;
+#pragma unroll
+                            for (int q = 0; q < WE; ++q) pj |= Sentinel<T>::is(v[j][q]);
+                            if ((++it & 255u) == 0 && wd_expired(t0)) break;
+                        } while (__any_sync(0xffffffffu, pj));
+                    }
+                    T c = br[(bs * UB + j) * 32 + lane];
+#pragma unroll
+                    for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
+                    if (((unsigned)code[j][0] & 0xE0000000u) == 0xE0000000u) {          // overflow list
+                        const T *ov = static_cast<const T *>(a.ovf_val);
+                        for (int o = code[j][0] & 0x1FFFFFFF;; ++o) {
+                            const int32_t cc = a.ovf_code[o];
+                            if (cc == kNone) break;
+                            T vv;
+                            if (code_kind(cc) == 1u) {
+                                vv = lds_volatile(slots + code_idx(cc));
+                                if (Sentinel<T>::is(vv)) vv = poll_smem_slow(slots + code_idx(cc));
+                            } else {
+                                vv = ld_relaxed_val(gm + code_idx(cc));
+                                if (Sentinel<T>::is(vv)) vv = poll_global_slow(gm + code_idx(cc));
+                            }
+                            c = fnma(ov[o], vv, c);
+                        }
+                    }
+                    sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
+                }
+            }
+            if (++rs == NBB) { rs = 0; rsph ^= 1; }
+            if (++rd == NBB) rd = 0;
+            if (++ro == RRB) ro = 0;
+            if (++rq == RRB) { rq = 0; rqph ^= 1; }
+            if (++bs == kBR) bs = 0;
+            if (++bw == kBR) bw = 0;
+            cs += UB;
+            if (cs == NCS) cs = 0;
+            cf += UB;
+            if (cf >= NCS) cf -= NCS;
         }
         cp_async_wait<0>();
-        if (trace && lane == 0) g_trace[(size_t)u * g_trace_cap + min(s1 - s0, g_trace_cap - 1)] = wd_now();
+    } else if (n > 0) {
+        // software-pipelined: the next step's c and record fields are loaded
+        // before this step's shuffle -> FMA chain; the readiness check of the
+        // next c comes after it (warp-uniform; fields reloaded if it was late)
+        T xprev = T(0);
+        auto wait_c = [&](T *cp) -> T {
+            T c = lds_volatile(cp);
+            if (__any_sync(0xffffffffu, Sentinel<T>::is(c))) {
+                const unsigned long long t0 = wd_now();
+                unsigned it = 0;
+                do {
+                    if (++it > 4) __nanosleep(20);          // leave the issue slots to the helper
+                    c = lds_volatile(cp);
+                    if ((it & 4095u) == 0 && wd_expired(t0)) break;
+                } while (__any_sync(0xffffffffu, Sentinel<T>::is(c)));
+            }
+            return c;
+        };
+        T *cp = cr + lane;
+        T c = wait_c(cp);
+        asm volatile("" ::: "memory");
+        const unsigned char *r = ring;
+        int4 ci = reinterpret_cast<const int4 *>(r)[lane];
+        CV<T> cv;
+        cv.load(r + CVO, lane);
+        int slot = 0;
+#pragma unroll 1
+        for (int t = 0; t < n; ++t) {
+            const int slot1 = slot + 1 == NCS ? 0 : slot + 1;
+            T *cp1 = cr + slot1 * 32 + lane;
+            const unsigned char *r1 = ring + (size_t)slot1 * REC;
+            T c1 = T(0);
+            int4 ci1 = make_int4(-1, -1, -1, 0);
+            CV<T> cv1;
+            const bool more = t + 1 < n;
+            if (more) {
+                c1 = lds_volatile(cp1);
+                asm volatile("" ::: "memory");
+                ci1 = reinterpret_cast<const int4 *>(r1)[lane];
+                cv1.load(r1 + CVO, lane);
+            }
+            const int nsh = ci.w & 7;
+            T acc = c;
+#pragma unroll
+            for (int q = 0; q < SH; ++q) {
+                const T vq = __shfl_sync(0xffffffffu, xprev, (ci.w >> (3 + 5 * q)) & 31);
+                acc = fnma(cv.v[1 + q], q < nsh ? vq : T(0), acc);
+            }
+            const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * cv.v[0];   // (a product is never the sentinel)
+            if (ci.x >= 0) __stcg(x + ci.x, xi);
+            if (ci.y >= 0) sts_flag(slots + ci.y, xi);
+            if (ci.z >= 0) stg_flag(gm + ci.z, xi);
+            sts_flag_last(cr + slot * 32 + lane, Sentinel<T>::value());     // step consumed: re-arm the c slot
+            xprev = xi;
+            if (more && __any_sync(0xffffffffu, Sentinel<T>::is(c1))) {     // the next c was not ready yet
+                c1 = wait_c(cp1);
+                asm volatile("" ::: "memory");
+                ci1 = reinterpret_cast<const int4 *>(r1)[lane];
+                cv1.load(r1 + CVO, lane);
+            }
+            c = c1;
+            ci = ci1;
+            cv = cv1;
+            slot = slot1;
+        }
     }
+
     __syncthreads();
     if (threadIdx.x == 0) {      // the last CTA to finish advances the mailbox epoch
         __threadfence();
@@ -664,18 +860,21 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
     }
 }
 
-// record width W (>= max dependencies, else overflow lists), UB steps per
-// block (registers: UB records live at once), BB blocks of b lookahead
-// record width W (>= max dependencies, else overflow lists), ub steps per
-// block (registers: ub records live at once)
+// per-tile shared memory of k_block (must match TILE there)
+size_t block_tile_bytes(int REC, int es, int ub) {
+    return ((size_t)kNBB * ub * REC + (size_t)kRRB * ub * 128 + (size_t)kNBB * ub * 32 * es +
+            (size_t)kBR * ub * 32 * es + 8 * (kNBB + kRRB) + 127) / 128 * 128;
+}
+
+// EXT entries per record row: enough for the detected-grid plans (7-point:
+// <= 2 EXT terms; 27-point: <= 13); more -> the overflow list
 template <typename T, bool UNIT>
-void *pick_kernel(int W, int &Wk, int &ub) {
-    if (W <= 3) { Wk = 3; ub = 4; return (void *)k_block<T, UNIT, 3, 4>; }
-    if (W <= 4) { Wk = 4; ub = 4; return (void *)k_block<T, UNIT, 4, 4>; }
-    if (W <= 8) { Wk = 8; ub = 2; return (void *)k_block<T, UNIT, 8, 2>; }
-    if (W <= 13) { Wk = 13; ub = 1; return (void *)k_block<T, UNIT, 13, 1>; }
-    Wk = 16; ub = 1;
-    return (void *)k_block<T, UNIT, 16, 1>;
+void *pick_kernel(int W, int &we) {
+    if (W <= 3) { we = 2; return (void *)k_block<T, UNIT, 2>; }
+    if (W <= 4) { we = 4; return (void *)k_block<T, UNIT, 4>; }
+    if (W <= 8) { we = 8; return (void *)k_block<T, UNIT, 8>; }
+    we = 13;
+    return (void *)k_block<T, UNIT, 13>;
 }
 bool g_host_trace = false;
 
@@ -785,22 +984,18 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
                                                 (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
     SPTRSV_CUDA(cudaGetLastError());
 
-    // kernel instance (record width W) and shared-memory budget
-    int Wk = 0, ub = 1;
-    const int W = std::max(1, std::min(h->info.max_row_deps, 16));
+    // kernel instance (EXT entries per record row) and shared-memory budget
+    int WE = 0;
+    const int W = std::max(1, h->info.max_row_deps);
     void *kn = nullptr;
     if (h->dtype == SPTRSV_F64)
-        kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(W, Wk, ub) : pick_kernel<double, false>(W, Wk, ub);
+        kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(W, WE) : pick_kernel<double, false>(W, WE);
     else
-        kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(W, Wk, ub) : pick_kernel<float, false>(W, Wk, ub);
-    // lookahead in blocks of ub steps: b gathered bb blocks ahead, records
-    // nb >= 2 bb blocks ahead (bb <= 8: cp.async.wait_group immediate)
-    const int bb = std::max(1, std::min(env_int("SPTRSV_BLOCK_BB", std::max(1, 8 / ub)), 8));
-    const int pb = bb * ub;          // steps of b ring per warp
-    const int REC = rec_bytes(Wk, (int)es);
+        kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(W, WE) : pick_kernel<float, false>(W, WE);
+    const int REC = rec_bytes(kSH, WE, (int)es);
     const size_t budget = (size_t)max_smem - 1024;          // static smem + slack
-    // per CTA: record rings (nst per warp) + b rings; the rest holds shared slots
-    auto ring_bytes = [&](int nw, int ns) { return (size_t)nw * ns * REC + (size_t)nw * pb * 32 * es; };
+    // per CTA (nt tiles): the tiles' rings; the rest holds shared slots
+    auto ring_bytes = [&](int nt) { return (size_t)nt * block_tile_bytes(REC, (int)es, ub_of(WE)); };
 
     // ---- 2. partition rows over U = K x wpc warps of K co-resident CTAs
     int32_t *unit = nullptr;
@@ -817,7 +1012,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         int tw = std::min(env_int("SPTRSV_BLOCK_TW", gny == 1 ? 32 : 8), gnx);
         int th = std::max(1, std::min(32 / std::max(tw, 1), gny));
         const int ewx = env_int("SPTRSV_BLOCK_WX", 0), ewy = env_int("SPTRSV_BLOCK_WY", 0);
-        static const int shapes[][2] = {{1, 1}, {2, 1}, {1, 2}, {2, 2}, {4, 2}, {2, 4}};
+        static const int shapes[][2] = {{1, 1}, {2, 1}, {1, 2}, {2, 2}};
         int wx = 0, wy = 0;
         for (int grow = 0; grow < 8 && wx == 0; ++grow) {
             const int ntx = (gnx + tw - 1) / tw, nty = (gny + th - 1) / th;
@@ -861,7 +1056,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         if (Kn <= 0) Kn = (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, n / 8192));
         K = std::min(Kn, h->num_sms);
         wpc = 4;
-        while (wpc > 1 && ring_bytes(wpc, 2 * pb) + 2048 * es > budget) wpc /= 2;
+        while (wpc > 1 && ring_bytes(wpc) + 2048 * es > budget) wpc /= 2;
         k_part_natural<<<eg, 256, 0, s>>>(n, K * wpc, h->uplo, unit);
     }
     SPTRSV_CUDA(cudaGetLastError());
@@ -914,14 +1109,14 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     SPTRSV_CUDA(cudaGetLastError());
 
     // ---- 4. shared-memory budget, dependency classes
-    int nst = std::max(env_int("SPTRSV_BLOCK_NST", 2 * pb), 2 * pb);
-    nst = (nst + ub - 1) / ub * ub;
-    auto fixed_bytes = [&](int ns) { return ring_bytes(wpc, ns); };
-    if (nst < 2 * pb || fixed_bytes(nst) > budget) return SPTRSV_ERR_NOT_SUPPORTED;
-    const int cap = (int)((budget - fixed_bytes(nst)) / es);
+    auto fixed_bytes = [&]() { return ring_bytes(wpc); };
+    if (fixed_bytes() > budget) return SPTRSV_ERR_NOT_SUPPORTED;
+    const int cap = (int)((budget - fixed_bytes()) / es);
 
     unsigned char *noslot = nullptr;
     int32_t *need = nullptr, *bits = nullptr, *slot_scan = nullptr, *g_scan = nullptr, *ccnt = nullptr;
+    int32_t *ecnt = nullptr;
+    if ((st = tmp.alloc_n(&ecnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&noslot, (size_t)K)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&need, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&bits, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
@@ -934,7 +1129,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     int max_slots = 0;
     for (int pass = 0; pass < 2; ++pass) {
         SPTRSV_CUDA(cudaMemsetAsync(need, 0, sizeof(int32_t) * ((size_t)n + 1), s));
-        k_need<<<eg, 256, 0, s>>>(n, Wk, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need);
+        k_need<<<eg, 256, 0, s>>>(n, kSH, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need, ecnt);
         k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
         if ((st = exclusive_scan_i32(bits, slot_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
         k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, ccnt);
@@ -978,15 +1173,16 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     int32_t *ocnt = nullptr, *ovf_ptr = nullptr;
     if ((st = tmp.alloc_n(&ocnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&ovf_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, Wk, bperm, tri_ptr, ocnt);
+    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, WE, ecnt, ocnt);
     if ((st = exclusive_scan_i32(ocnt, ovf_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     const int32_t novf = i32_at(ovf_ptr, n, s, st);
     if (st != SPTRSV_SUCCESS) return st;
     B.novf = novf;
-    // + 16 padding steps (0xFF: row -1, codes NONE) so a warp's last block of ub
-    // records can be read whole
-    if ((st = h->arena.alloc(&B.d_recs, (size_t)((int64_t)nsteps + 16) * REC)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync((unsigned char *)B.d_recs + (size_t)nsteps * REC, 0xFF, (size_t)16 * REC, s));
+    // + 4 padding steps: a warp's last block of records / row ids is copied whole
+    if ((st = h->arena.alloc(&B.d_recs, (size_t)((int64_t)nsteps + 4) * REC)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_rows, (size_t)((int64_t)nsteps + 4) * 32)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync((unsigned char *)B.d_recs + (size_t)nsteps * REC, 0xFF, (size_t)4 * REC, s));
+    SPTRSV_CUDA(cudaMemsetAsync(B.d_rows + (size_t)nsteps * 32, 0xFF, (size_t)4 * 128, s));
     if ((st = h->arena.alloc_n(&B.d_ovf_code, (size_t)std::max(novf, 1))) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc(&B.d_ovf_val, (size_t)std::max(novf, 1) * es)) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc(&B.d_gmb, (size_t)2 * std::max(G, 1) * es)) != SPTRSV_SUCCESS) return st;
@@ -995,32 +1191,33 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     const int pg = (int)std::max<int64_t>(1, ((int64_t)nsteps * 32 + 255) / 256);
     const int fg = std::max(1, std::min((int)((2 * (int64_t)std::max(G, 1) + 255) / 256), h->num_sms * 8));
     if (h->dtype == SPTRSV_F64) {
-        k_rec_fill<double><<<pg, 256, 0, s>>>(nsteps, Wk, wpc, steps, step_unit, bperm, pos, step_of, unit, tri_ptr,
-                                              tri_col, (const double *)tri_val, (const double *)h->d_invd_row, noslot,
-                                              need, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
-                                              B.d_ovf_code, (double *)B.d_ovf_val);
+        k_rec_fill<double><<<pg, 256, 0, s>>>(nsteps, kSH, WE, wpc, steps, bperm, pos, step_of, unit, tri_ptr,
+                                              tri_col, (const double *)tri_val, (const double *)h->d_invd_row,
+                                              h->diag == SPTRSV_UNIT, noslot, need, ecnt, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
+                                              B.d_rows, B.d_ovf_code, (double *)B.d_ovf_val);
         k_fill_sentinel<double><<<fg, 256, 0, s>>>((double *)B.d_gmb, 2 * (int64_t)std::max(G, 1));
     } else {
-        k_rec_fill<float><<<pg, 256, 0, s>>>(nsteps, Wk, wpc, steps, step_unit, bperm, pos, step_of, unit, tri_ptr,
-                                             tri_col, (const float *)tri_val, (const float *)h->d_invd_row, noslot,
-                                             need, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
-                                             B.d_ovf_code, (float *)B.d_ovf_val);
+        k_rec_fill<float><<<pg, 256, 0, s>>>(nsteps, kSH, WE, wpc, steps, bperm, pos, step_of, unit, tri_ptr,
+                                             tri_col, (const float *)tri_val, (const float *)h->d_invd_row,
+                                             h->diag == SPTRSV_UNIT, noslot, need, ecnt, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
+                                             B.d_rows, B.d_ovf_code, (float *)B.d_ovf_val);
         k_fill_sentinel<float><<<fg, 256, 0, s>>>((float *)B.d_gmb, 2 * (int64_t)std::max(G, 1));
     }
     SPTRSV_CUDA(cudaGetLastError());
 
-    // ---- launch configuration: K co-resident CTAs of wpc warps
-    const size_t smem = fixed_bytes(nst) + (size_t)max_slots * es;
+    // ---- launch configuration: K co-resident CTAs of wpc tiles (2 warps each)
+    const size_t smem = fixed_bytes() + (size_t)max_slots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 32 * wpc, smem));
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 64 * wpc, smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = 32 * wpc;
-    B.nst = nst;
-    B.bb = bb;
-    B.W = Wk;
+    B.threads = 64 * wpc;
+    B.nst = kNBB * ub_of(WE);
+    B.bb = kR2B * ub_of(WE);
+    B.d = kDB * ub_of(WE);
+    B.W = WE;
     B.rec_bytes = REC;
     B.nent = (int64_t)nsteps * REC;
     SPTRSV_CUDA(cudaStreamSynchronize(s));
@@ -1034,6 +1231,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     BlockArgs a;
     a.unit_step0 = B.d_unit_step0;
     a.recs = (const unsigned char *)B.d_recs;
+    a.rows = B.d_rows;
     a.cta_g0 = B.d_cta_g0;
     a.ovf_code = B.d_ovf_code;
     a.ovf_val = B.d_ovf_val;
@@ -1042,9 +1240,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     a.b = b;
     a.x = x;
     a.G = B.G;
-    a.nst = B.nst;
     a.nslots = B.nslots;
-    a.bb = B.bb;
     void *args[] = {(void *)&a};
     SPTRSV_CUDA(cudaLaunchCooperativeKernel(B.kernel, B.nblocks, B.threads, args, B.smem, s));
     return SPTRSV_SUCCESS;

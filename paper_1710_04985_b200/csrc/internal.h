@@ -34,11 +34,13 @@ struct DevArena {
 struct BlockPlan {
     bool built = false;
     int32_t nblocks = 0;      // K co-resident CTAs
-    int32_t wpc = 0;          // warps per CTA
-    int32_t nunits = 0;       // K x wpc warps
-    int32_t W = 0;            // record entries per row (kernel instance)
+    int32_t wpc = 0;          // tiles per CTA
+    int32_t nunits = 0;       // K x wpc tiles (a compute and a helper warp each)
+    int32_t W = 0;            // EXT entries per record row (kernel instance)
     int32_t nst = 0;          // record ring per warp (steps)
-    int32_t bb = 0;           // b lookahead (blocks)
+    int32_t bb = 0;           // b lookahead (steps)
+    int32_t d = 0;            // record lookahead (steps)
+    int32_t r1 = 0, rr = 0;   // row-id lookahead / ring (steps)
     int32_t nsteps = 0;       // (warp, level) steps of <= 32 rows
     int32_t G = 0;            // global mailboxes (values read by another CTA)
     int32_t nslots = 0;       // shared slots per CTA (values read by another warp of the CTA)
@@ -49,6 +51,7 @@ struct BlockPlan {
     void *kernel = nullptr;
     int32_t *d_unit_step0 = nullptr;  // [U+1] first step of every warp
     void *d_recs = nullptr;           // step records (see block.cu)
+    int32_t *d_rows = nullptr;        // [nsteps][32] row ids (b gather addresses)
     int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
     int32_t *d_ovf_code = nullptr;    // overflow entries (rows with > W dependencies)
     void *d_ovf_val = nullptr;
