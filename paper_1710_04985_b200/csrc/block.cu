@@ -999,7 +999,8 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
 
     // ---- 2. partition rows over U = K x wpc warps of K co-resident CTAs
     int32_t *unit = nullptr;
-    if ((st = tmp.alloc_n(&unit, n)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&unit, n)) != SPTRSV_SUCCESS) return st;
+    B.d_unit = unit;
     int gnx = 0, gny = 0;
     if (n >= 64 && !env_int("SPTRSV_BLOCK_NO_GRID", 0)) {
         if ((st = detect_grid(h, tri_ptr, tri_col, tmp, s, gnx, gny)) != SPTRSV_SUCCESS) return st;
@@ -1222,6 +1223,144 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     B.nent = (int64_t)nsteps * REC;
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     B.built = true;
+    return SPTRSV_SUCCESS;
+}
+
+// ---------------------------------------------------------------- CTA-tile multi-RHS plan
+// Positions sorted by (CTA, level, row) with the BLOCK partition's CTAs; a
+// per-position CSR (same shape as the level-ordered multi-RHS CSR, so the
+// row kernels are shared); per (CTA, level) position ranges; per CTA the list
+// of CTAs that produce its dependencies.  k_tile_mrhs (solve.cu) walks each
+// CTA's levels with __syncthreads between them and waits only for its
+// producer CTAs' level counters: no grid-wide barrier.
+__global__ void k_tm_keys(int n, int nlev, int wpc, const int32_t *unit, const int32_t *lev, uint32_t *keys,
+                          int32_t *cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = (uint32_t)(unit[i] / wpc) * (uint32_t)nlev + (uint32_t)lev[i];
+    keys[i] = k;
+    atomicAdd(&cnt[k], 1);
+}
+
+template <typename T>
+__global__ void k_tm_rows(int n, const int32_t *perm, const int32_t *dp, const T *invd_row, int unit_diag,
+                          T *invd, int32_t *deg) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) {
+        const int i = perm[p];
+        invd[p] = unit_diag ? T(1) : invd_row[i];
+        deg[p] = dp[i];
+    }
+    if (p == n) deg[p] = 0;
+}
+
+template <typename T>
+__global__ void k_tm_fill(int n, int K, int wpc, const int32_t *perm, const int32_t *tri_ptr, const int32_t *tri_col,
+                          const T *tri_val, const int32_t *unit, const int32_t *ptr, int32_t *col, T *val,
+                          unsigned char *depm) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int i = perm[p];
+    const int ci = unit[i] / wpc;
+    int o = ptr[p];
+    for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k, ++o) {
+        const int j = tri_col[k];
+        col[o] = j;
+        val[o] = tri_val[k];
+        const int cj = unit[j] / wpc;
+        if (cj != ci) depm[(size_t)ci * K + cj] = 1;
+    }
+}
+
+sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s) {
+    BlockPlan &B = h->block;
+    if (!B.built || B.grid_nx == 0) return SPTRSV_ERR_NOT_SUPPORTED;
+    const int n = h->n, nlev = h->info.nlev, K = B.nblocks, wpc = B.wpc;
+    const size_t es = h->esize;
+    if ((uint64_t)K * (uint64_t)nlev >= (1ull << 31)) return SPTRSV_ERR_NOT_SUPPORTED;
+    DevArena tmp;
+    struct Guard {
+        DevArena &a;
+        ~Guard() { a.release_all(); }
+    } guard{tmp};
+    sptrsv_status_t st;
+    const int eg = (n + 256) / 256;
+    // natural-order CSR of the triangle (as in block_build)
+    int32_t *tri_ptr = nullptr, *tri_col = nullptr, *dpx = nullptr;
+    void *tri_val = nullptr;
+    const int64_t nnz = std::max<int64_t>(h->info.nnz_used, 1);
+    if ((st = tmp.alloc_n(&tri_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&tri_col, (size_t)nnz)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc(&tri_val, (size_t)nnz * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&dpx, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemcpyAsync(dpx, h->d_dp, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+    SPTRSV_CUDA(cudaMemsetAsync(dpx + n, 0, sizeof(int32_t), s));
+    if ((st = exclusive_scan_i32(dpx, tri_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    const int cgrid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
+    if (h->dtype == SPTRSV_F64)
+        k_tri_fill<double><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
+                                                 (const double *)h->d_eval, tri_ptr, tri_col, (double *)tri_val);
+    else
+        k_tri_fill<float><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
+                                                (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
+    // order by (CTA, level, row); (CTA, level) offsets
+    const int64_t KL = (int64_t)K * nlev;
+    uint32_t *keys = nullptr, *skeys = nullptr;
+    int32_t *cnt = nullptr, *deg = nullptr;
+    unsigned char *depm = nullptr;
+    if ((st = tmp.alloc_n(&keys, n)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&skeys, n)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&cnt, (size_t)KL + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&deg, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&depm, (size_t)K * K)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_perm, n)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc(&B.d_tm_invd, (size_t)n * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_col, (size_t)nnz)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc(&B.d_tm_val, (size_t)nnz * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_off, (size_t)KL + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_done, (size_t)K)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)KL + 1), s));
+    SPTRSV_CUDA(cudaMemsetAsync(depm, 0, (size_t)K * K, s));
+    SPTRSV_CUDA(cudaMemsetAsync(B.d_tm_done, 0, sizeof(unsigned long long) * K, s));
+    k_tm_keys<<<eg, 256, 0, s>>>(n, nlev, wpc, B.d_unit, h->d_lev, keys, cnt);
+    if ((st = radix_sort_pairs(keys, nullptr, skeys, B.d_tm_perm, n, (uint32_t)(KL - 1), tmp, s)) != SPTRSV_SUCCESS)
+        return st;
+    if ((st = exclusive_scan_i32(cnt, B.d_tm_off, (int64_t)KL + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    if (h->dtype == SPTRSV_F64)
+        k_tm_rows<double><<<eg, 256, 0, s>>>(n, B.d_tm_perm, h->d_dp, (const double *)h->d_invd_row,
+                                             h->diag == SPTRSV_UNIT, (double *)B.d_tm_invd, deg);
+    else
+        k_tm_rows<float><<<eg, 256, 0, s>>>(n, B.d_tm_perm, h->d_dp, (const float *)h->d_invd_row,
+                                            h->diag == SPTRSV_UNIT, (float *)B.d_tm_invd, deg);
+    if ((st = exclusive_scan_i32(deg, B.d_tm_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    if (h->dtype == SPTRSV_F64)
+        k_tm_fill<double><<<eg, 256, 0, s>>>(n, K, wpc, B.d_tm_perm, tri_ptr, tri_col, (const double *)tri_val,
+                                             B.d_unit, B.d_tm_ptr, B.d_tm_col, (double *)B.d_tm_val, depm);
+    else
+        k_tm_fill<float><<<eg, 256, 0, s>>>(n, K, wpc, B.d_tm_perm, tri_ptr, tri_col, (const float *)tri_val,
+                                            B.d_unit, B.d_tm_ptr, B.d_tm_col, (float *)B.d_tm_val, depm);
+    SPTRSV_CUDA(cudaGetLastError());
+    // producer lists
+    std::vector<unsigned char> hdep((size_t)K * K);
+    SPTRSV_CUDA(cudaMemcpyAsync(hdep.data(), depm, (size_t)K * K, cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> dptr(K + 1, 0), dl;
+    for (int c = 0; c < K; ++c) {
+        for (int p = 0; p < K; ++p)
+            if (hdep[(size_t)c * K + p]) dl.push_back(p);
+        dptr[c + 1] = (int32_t)dl.size();
+    }
+    if (dl.empty()) dl.push_back(0);
+    if ((st = h->arena.alloc_n(&B.d_tm_dptr, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_tm_dl, dl.size())) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemcpyAsync(B.d_tm_dptr, dptr.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    SPTRSV_CUDA(cudaMemcpyAsync(B.d_tm_dl, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    B.tm_K = K;
+    B.tm_base = 0;
+    B.tm_built = true;
+    h->info.device_bytes = h->arena.bytes;
     return SPTRSV_SUCCESS;
 }
 

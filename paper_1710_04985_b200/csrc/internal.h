@@ -57,6 +57,20 @@ struct BlockPlan {
     void *d_ovf_val = nullptr;
     void *d_gmb = nullptr;            // [2][G] mailboxes (value-as-flag), roles swap per solve
     unsigned *d_ctr = nullptr;        // [0] solve epoch, [1] finished CTAs
+    int32_t *d_unit = nullptr;        // [n] warp tile of every row (CTA = unit / wpc)
+    // CTA-tile multi-RHS plan (built on the first multi-RHS BLOCK solve; see block.cu)
+    bool tm_built = false;
+    int32_t tm_K = 0;
+    int32_t *d_tm_perm = nullptr;     // [n] position -> row, positions sorted by (CTA, level, row)
+    void *d_tm_invd = nullptr;        // [n] 1/d by position
+    int32_t *d_tm_ptr = nullptr;      // [n+1] CSR of the referenced strict triangle by position
+    int32_t *d_tm_col = nullptr;
+    void *d_tm_val = nullptr;
+    int32_t *d_tm_off = nullptr;      // [K*nlev+1] first position of (CTA, level)
+    int32_t *d_tm_dptr = nullptr;     // [K+1] producer-CTA lists
+    int32_t *d_tm_dl = nullptr;
+    unsigned long long *d_tm_done = nullptr;   // [K] levels completed (epoch based, monotone)
+    unsigned long long tm_base = 0;
 };
 
 }  // namespace sptrsv
@@ -115,6 +129,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
+sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s);
 // device scans (analyze.cu)
 sptrsv_status_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
 sptrsv_status_t exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, DevArena &tmp, cudaStream_t s);

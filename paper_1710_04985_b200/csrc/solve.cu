@@ -193,9 +193,10 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *bar, unsigned l
     __syncthreads();
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
-        while (ld_relaxed_u64(bar) < target) {
+        // acquire polls: no separate fence after the wait (a fence.acq_rel
+        // costs ~150-580 ns on B200, profiles/microbench_r1.json)
+        while (ld_acquire_u64(bar) < target) {
         }
-        fence_acq_rel_gpu();
     }
     __syncthreads();
 }
@@ -402,10 +403,32 @@ __device__ __forceinline__ void mr_load(MrRow<T, CPL> &R, int p, int lane, const
 template <typename T, bool UNIT, int CPL>
 __device__ __forceinline__ void mr_solve(const MrRow<T, CPL> &R, int lane, const int32_t *__restrict__ mr_col,
                                          const T *__restrict__ mr_val, T *x, int nrhs) {
+    // the x rows of the first kBatch dependencies are loaded together (one
+    // memory latency instead of one per dependency); the FMAs then run in
+    // storage order, as before
+    constexpr int kBatch = 4;
     T acc[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; ++j) acc[j] = R.bv[j];
-    for (int k = 0; k < R.deg; ++k) {
+    T xv[kBatch][CPL];
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+        const int ck = __shfl_sync(0xffffffffu, R.col, k);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const int c = lane + 32 * j;
+            xv[k][j] = (k < R.deg && c < nrhs) ? ld_cg(x + (int64_t)ck * nrhs + c) : T(0);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+        const T vk = __shfl_sync(0xffffffffu, R.val, k);
+        if (k < R.deg) {
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) acc[j] = fnma(vk, xv[k][j], acc[j]);
+        }
+    }
+    for (int k = kBatch; k < R.deg; ++k) {
         const int ck = k < 32 ? __shfl_sync(0xffffffffu, R.col, k) : mr_col[R.e0 + k];
         const T vk = k < 32 ? __shfl_sync(0xffffffffu, R.val, k) : mr_val[R.e0 + k];
 #pragma unroll
@@ -445,11 +468,15 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
     }
     for (int l = 0; l < nlev; ++l) {
         const int p0 = ilev[l], p1 = ilev[l + 1];
-        if (have) mr_solve<T, UNIT, CPL>(pre, lane, mr_col, mr_val, x, nrhs);
-        for (int p = p0 + gw + nw; p < p1; p += nw) {      // further rows of this level (wide levels)
-            MrRow<T, CPL> R;
-            mr_load(R, p, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
-            mr_solve<T, UNIT, CPL>(R, lane, mr_col, mr_val, x, nrhs);
+        // further rows of this level (wide levels): the next row's metadata and
+        // b are loaded before the current row is solved
+        for (int p = p0 + gw; have; p += nw) {
+            MrRow<T, CPL> nxt;
+            const bool more = p + nw < p1;
+            if (more) mr_load(nxt, p + nw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+            mr_solve<T, UNIT, CPL>(pre, lane, mr_col, mr_val, x, nrhs);
+            if (!more) break;
+            pre = nxt;
         }
         if (l + 1 < nlev) {
             have = 0;
@@ -461,6 +488,72 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
             grid_barrier(bar, bar_base + (unsigned long long)(l + 1) * gridDim.x);
         }
     }
+}
+
+// Multi-RHS over the BLOCK partition's CTAs (tile_mrhs_build, block.cu): CTA c
+// walks its non-empty levels in order; within a level its warps take rows
+// (lanes over right-hand sides, the next row's metadata and b loaded before
+// the current row is solved), __syncthreads, then thread 0 publishes the next
+// level it will work on (release).  Before a level l, one thread per producer
+// CTA waits (acquire) until that CTA's counter reaches l: every dependency of
+// a level-l row has a lower level, so no grid-wide barrier is
+// needed and a CTA runs ahead of the ones that do not feed it.
+constexpr int kTileThreads = 512;
+template <typename T, bool UNIT, int CPL>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    k_tile_mrhs(int nlev, const int32_t *__restrict__ off, const int32_t *__restrict__ dptr,
+                const int32_t *__restrict__ dl, unsigned long long *done, unsigned long long base,
+                const int32_t *__restrict__ perm, const T *__restrict__ invd, const int32_t *__restrict__ ptr,
+                const int32_t *__restrict__ col, const T *__restrict__ val, const T *b, T *x, int nrhs) {
+    const int c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int32_t *co = off + (size_t)c * nlev;        // co[l] .. co[l+1]: positions of (c, l)
+    auto next_level = [&](int l) {                      // first non-empty level >= l (nlev if none)
+        while (l < nlev && co[l] == co[l + 1]) ++l;
+        return l;
+    };
+    int l = next_level(0);
+    if (threadIdx.x == 0) st_release_u64(&done[c], base + (unsigned long long)l);
+    const int d0 = dptr[c], nd = dptr[c + 1] - d0;
+    while (l < nlev) {
+        for (int q = threadIdx.x; q < nd; q += blockDim.x) {
+            const unsigned long long *f = &done[dl[d0 + q]];
+            const unsigned long long target = base + (unsigned long long)l;
+            while (ld_acquire_u64(f) < target) {
+            }
+        }
+        __syncthreads();
+        const int p1 = co[l + 1];
+        int p = co[l] + warp;
+        if (p < p1) {
+            MrRow<T, CPL> cur;
+            mr_load(cur, p, lane, perm, invd, ptr, col, val, b, nrhs);
+            for (;; p += nw) {
+                MrRow<T, CPL> nxt;
+                const bool more = p + nw < p1;
+                if (more) mr_load(nxt, p + nw, lane, perm, invd, ptr, col, val, b, nrhs);
+                mr_solve<T, UNIT, CPL>(cur, lane, col, val, x, nrhs);
+                if (!more) break;
+                cur = nxt;
+            }
+        }
+        __syncthreads();
+        l = next_level(l + 1);
+        if (threadIdx.x == 0) st_release_u64(&done[c], base + (unsigned long long)l);
+    }
+}
+
+template <typename T, bool UNIT, int CPL>
+sptrsv_status_t launch_tile_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
+    BlockPlan &B = h->block;
+    const int nlev = h->info.nlev;
+    unsigned long long base = B.tm_base;
+    void *args[] = {(void *)&nlev, (void *)&B.d_tm_off, (void *)&B.d_tm_dptr, (void *)&B.d_tm_dl,
+                    (void *)&B.d_tm_done, (void *)&base, (void *)&B.d_tm_perm, (void *)&B.d_tm_invd,
+                    (void *)&B.d_tm_ptr, (void *)&B.d_tm_col, (void *)&B.d_tm_val, (void *)&b, (void *)&x,
+                    (void *)&nrhs};
+    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_tile_mrhs<T, UNIT, CPL>, B.tm_K, kTileThreads, args, 0, s));
+    B.tm_base += (unsigned long long)nlev + 1;
+    return SPTRSV_SUCCESS;
 }
 
 // per-position CSR of the referenced strict triangle (multi-RHS layout)
@@ -609,6 +702,16 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         if (!h->mr_built) {
             sptrsv_status_t st = build_mr<T>(h, s);
             if (st != SPTRSV_SUCCESS) return st;
+        }
+        if (h->algo == SPTRSV_ALGO_BLOCK && !h->block.tm_built && h->block.built && h->block.grid_nx > 0) {
+            sptrsv_status_t st = tile_mrhs_build(h, s);
+            if (st != SPTRSV_SUCCESS) return st;
+        }
+        if (h->algo == SPTRSV_ALGO_BLOCK && h->block.tm_built) {
+            if (nrhs <= 32) return launch_tile_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
+            if (nrhs <= 64) return launch_tile_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
+            if (nrhs <= 128) return launch_tile_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
+            return SPTRSV_ERR_NOT_SUPPORTED;
         }
         const bool lv = h->algo == SPTRSV_ALGO_LEVEL;
         if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);

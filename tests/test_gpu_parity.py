@@ -238,7 +238,25 @@ def test_multi_rhs_small(S, nrhs, algo):
         assert relerr(x, oracle.solve(m, b, uplo)) <= 1e-10
 
 
-@pytest.mark.parametrize("algo", ["self", "level"])
+@pytest.mark.parametrize("nrhs", [2, 17, 64, 100])
+@pytest.mark.parametrize("case", ["7pt_lower", "7pt_upper", "27pt_lower_unit", "5pt_2d"])
+def test_multi_rhs_tiles(S, case, nrhs):
+    # BLOCK on detected grids: the CTA-tile multi-RHS kernel (producer-CTA waits)
+    if case == "7pt_lower":
+        m, uplo, diag = workloads.stencil((24, 20, 12), 7, "lower"), "lower", "non_unit"
+    elif case == "7pt_upper":
+        m, uplo, diag = workloads.stencil((24, 20, 12), 7, "upper"), "upper", "non_unit"
+    elif case == "27pt_lower_unit":
+        m, uplo, diag = workloads.ilu0(workloads.stencil((12, 10, 8), 27)), "lower", "unit"
+    else:
+        m, uplo, diag = workloads.stencil((64, 48), 5, "lower"), "lower", "non_unit"
+    b = workloads.rhs(m.n, nrhs, seed=nrhs + 7)
+    x, sv = gpu_solve(S, m, b, uplo=uplo, diag=diag, algo="block")
+    assert sv.info()["nblocks"] > 0
+    assert relerr(x, oracle.solve(m, b, uplo, diag)) <= 1e-10
+
+
+@pytest.mark.parametrize("algo", ["self", "level", "block"])
 def test_cfg5_full_64_rhs_and_partition_bitwise(S, algo):
     # cfg5: 64 RHS on the 128^3 factor; column blocks (G = 2, 4, 8) must equal
     # the G = 1 columns bit for bit, and match the oracle
