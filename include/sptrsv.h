@@ -58,8 +58,11 @@ typedef enum {
     SPTRSV_ALGO_LEVEL = 1,  /* level-scheduled, grid-wide barrier per level (LEVR) */
     SPTRSV_ALGO_BLOCK = 2,  /* self-scheduled over warp-owned row tiles, register/shared-memory
                                hand-offs (any matrix, fastest on structured grids) */
-    SPTRSV_ALGO_AUTO = 3    /* BLOCK when the analysis detects a structured grid, else SELF;
+    SPTRSV_ALGO_AUTO = 3,   /* BLOCK when the analysis detects a structured grid, else SELF;
                                info.algo then reports the algorithm chosen */
+    SPTRSV_ALGO_TILE = 4    /* CTA tiles: level-synchronous inside a CTA (x in shared memory),
+                               producer-CTA level counters between CTAs;
+                               structured grids with <= 3 dependencies per row */
 } sptrsv_algo_t;
 
 typedef enum {

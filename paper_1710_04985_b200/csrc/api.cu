@@ -146,17 +146,27 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
 extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
     if (!h) return SPTRSV_ERR_INVALID_VALUE;
     if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK &&
-        algo != SPTRSV_ALGO_AUTO)
+        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_TILE)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
-    if ((algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_AUTO) && !h->block.built && h->n > 0) {
+    const bool want_block = algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_AUTO || algo == SPTRSV_ALGO_TILE;
+    if (want_block && !h->block.built && h->n > 0) {
         SPTRSV_CUDA(cudaSetDevice(h->device));
         sptrsv_status_t st = block_build(h, nullptr);
-        if (st != SPTRSV_SUCCESS && algo == SPTRSV_ALGO_BLOCK) return st;
+        if (st != SPTRSV_SUCCESS && algo != SPTRSV_ALGO_AUTO) return st;
         h->info.nblocks = h->block.built ? h->block.nblocks : 0;
         h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
     }
-    if (algo == SPTRSV_ALGO_AUTO)
+    if (algo == SPTRSV_ALGO_TILE && !h->tile.built && h->n > 0 &&
+        h->block.built && h->block.grid_nx > 0) {
+        SPTRSV_CUDA(cudaSetDevice(h->device));
+        sptrsv_status_t st = h->block.tm_built ? SPTRSV_SUCCESS : tile_mrhs_build(h, nullptr);
+        if (st == SPTRSV_SUCCESS) st = tile_build(h, nullptr);
+        if (st != SPTRSV_SUCCESS && algo == SPTRSV_ALGO_TILE) return st;
+        h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
+    }
+    if (algo == SPTRSV_ALGO_TILE && !h->tile.built) return SPTRSV_ERR_NOT_SUPPORTED;
+    if (algo == SPTRSV_ALGO_AUTO)     // BLOCK is the fastest single-RHS path on grids (profiles/)
         algo = (h->block.built && h->block.grid_nx > 0) ? SPTRSV_ALGO_BLOCK : SPTRSV_ALGO_SELF;
     h->algo = algo;
     h->info.algo = algo;

@@ -73,6 +73,21 @@ struct BlockPlan {
     unsigned long long tm_base = 0;
 };
 
+// CTA-tile level-synchronous plan (SPTRSV_ALGO_TILE); see tile.cu.
+struct TilePlan {
+    bool built = false;
+    int32_t K = 0, threads = 0, maxr = 0;
+    size_t smem = 0;
+    void *kernel = nullptr;
+    int4 *d_clist = nullptr;          // per CTA non-empty levels {level, first position, rows, 0}
+    int32_t *d_cptr = nullptr;        // [K+1]
+    int32_t *d_cpos = nullptr;        // [K+1] first position of every CTA
+    int4 *d_ri = nullptr;             // [n] {row, code0..2}
+    void *d_rv = nullptr;             // [n][4] {1/d, v0..v2}
+    unsigned long long *d_done = nullptr;   // [K] level counters (epoch based)
+    unsigned long long base = 0;
+};
+
 }  // namespace sptrsv
 
 struct sptrsv_handle_s {
@@ -121,6 +136,7 @@ struct sptrsv_handle_s {
     void *d_scratch = nullptr;               // copy of b for in-place value-as-flag solves
     size_t scratch_bytes = 0;
     sptrsv::BlockPlan block;
+    sptrsv::TilePlan tile;
 };
 
 namespace sptrsv {
@@ -130,6 +146,8 @@ sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nr
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
 sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s);
+sptrsv_status_t tile_build(sptrsv_handle_t h, cudaStream_t s);
+sptrsv_status_t tile_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
 // device scans (analyze.cu)
 sptrsv_status_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
 sptrsv_status_t exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, DevArena &tmp, cudaStream_t s);

@@ -22,6 +22,8 @@
 // k_level reduce lane partial sums with a fixed shuffle tree.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace sptrsv {
@@ -703,17 +705,21 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             sptrsv_status_t st = build_mr<T>(h, s);
             if (st != SPTRSV_SUCCESS) return st;
         }
-        if (h->algo == SPTRSV_ALGO_BLOCK && !h->block.tm_built && h->block.built && h->block.grid_nx > 0) {
+        // CTA-tile multi-RHS (k_tile_mrhs) on request (env SPTRSV_MRHS_TILE=1):
+        // on cfg5 the level-scheduled multi-RHS kernel is faster (profiles/)
+        const char *ev = getenv("SPTRSV_MRHS_TILE");
+        const bool tiled = (h->algo == SPTRSV_ALGO_BLOCK || h->algo == SPTRSV_ALGO_TILE) && ev && *ev == '1';
+        if (tiled && !h->block.tm_built && h->block.built && h->block.grid_nx > 0) {
             sptrsv_status_t st = tile_mrhs_build(h, s);
             if (st != SPTRSV_SUCCESS) return st;
         }
-        if (h->algo == SPTRSV_ALGO_BLOCK && h->block.tm_built) {
+        if (tiled && h->block.tm_built) {
             if (nrhs <= 32) return launch_tile_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
             if (nrhs <= 64) return launch_tile_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
             if (nrhs <= 128) return launch_tile_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
             return SPTRSV_ERR_NOT_SUPPORTED;
         }
-        const bool lv = h->algo == SPTRSV_ALGO_LEVEL;
+        const bool lv = h->algo != SPTRSV_ALGO_SELF;     // BLOCK / TILE: level-scheduled multi-RHS
         if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
         if (nrhs <= 64) return lv ? launch_level_mrhs<T, UNIT, 2>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
         if (nrhs <= 128) return lv ? launch_level_mrhs<T, UNIT, 4>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
@@ -728,6 +734,7 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
 
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s) {
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_BLOCK) return block_solve(h, b, x, s);
+    if (nrhs == 1 && h->algo == SPTRSV_ALGO_TILE) return tile_solve(h, b, x, s);
     if (h->dtype == SPTRSV_F64) {
         return h->diag == SPTRSV_UNIT ? launch<double, true>(h, (const double *)b, (double *)x, nrhs, s)
                                       : launch<double, false>(h, (const double *)b, (double *)x, nrhs, s);

@@ -20,7 +20,7 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
 
 TOL = {np.float64: 1e-10, np.float32: 1e-4}
-ALGOS = ["self", "level", "block"]
+ALGOS = ["self", "level", "block", "auto"]
 
 
 @pytest.fixture(scope="module")
@@ -240,8 +240,9 @@ def test_multi_rhs_small(S, nrhs, algo):
 
 @pytest.mark.parametrize("nrhs", [2, 17, 64, 100])
 @pytest.mark.parametrize("case", ["7pt_lower", "7pt_upper", "27pt_lower_unit", "5pt_2d"])
-def test_multi_rhs_tiles(S, case, nrhs):
+def test_multi_rhs_tiles(S, case, nrhs, monkeypatch):
     # BLOCK on detected grids: the CTA-tile multi-RHS kernel (producer-CTA waits)
+    monkeypatch.setenv("SPTRSV_MRHS_TILE", "1")
     if case == "7pt_lower":
         m, uplo, diag = workloads.stencil((24, 20, 12), 7, "lower"), "lower", "non_unit"
     elif case == "7pt_upper":
@@ -336,3 +337,42 @@ def test_invalid_value_and_empty(S):
     b = torch.zeros(m2.n, dtype=torch.float64, device="cuda")
     assert S.sptrsv_solve(sv2.handle, S._dptr(b), S._dptr(b), 0, None) == 1   # nrhs < 1
     assert S.sptrsv_set_algo(sv2.handle, 9) == 1
+
+
+# ------------------------------------------------------------ TILE (CTA tiles, grids)
+TILE_CASES = [((32, 32), 5, "lower"), ((64, 48), 5, "upper"), ((16, 16, 16), 7, "lower"),
+              ((40, 30, 20), 7, "lower"), ((40, 30, 20), 7, "upper"), ((128, 128, 128), 7, "lower")]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("dims,pts,uplo", TILE_CASES)
+def test_tile_solve_grids(S, dims, pts, uplo, dtype):
+    m = workloads.stencil(dims, pts, uplo)
+    b = workloads.rhs(m.n, 1, seed=len(dims) * 10 + pts)[:, 0]
+    ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, dtype=dtype)
+    x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="tile")
+    assert sv.info()["algo"] == 4
+    assert relerr(x, ref) <= TOL[dtype]
+    x2, _ = gpu_solve(S, m, b, dtype=dtype, solver=sv)   # run-to-run bitwise (epoch counters advance)
+    assert np.array_equal(x, x2)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("uplo", ["lower", "upper"])
+def test_tile_integer_exact_and_in_place(S, uplo, dtype):
+    m = workloads.stencil((40, 30, 20), 7, uplo, diag=8.0)
+    xt = workloads.integer_xtrue(m.n, 1, seed=101)[:, 0]
+    b = oracle.matvec(m, xt, uplo)
+    x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="tile")
+    assert np.array_equal(x.astype(np.float64), xt)
+    bt = torch.from_numpy(b.astype(dtype)).cuda()
+    sv.solve(bt, x=bt)
+    assert np.array_equal(bt.cpu().numpy().astype(np.float64), xt)
+
+
+def test_tile_not_supported_off_grid(S):
+    m = random_triangular_fast(3000, 4.0, 3, "lower")
+    with pytest.raises(S.SptrsvError):
+        S.from_csr(m, algo="tile")
+    sv = S.from_csr(m, algo="auto")                  # auto falls back to SELF off grids
+    assert sv.info()["algo"] == 0
