@@ -534,10 +534,10 @@ __device__ __forceinline__ void mbar_wait_wd(uint64_t *bar, uint32_t ph) {
 // -> FMA chain -> multiply.  The helper runs at most (NBB - DB) blocks ahead:
 // record slot k+DB reuses the slot of block k+DB-NBB, free once the compute
 // warp re-armed the c slot of that block's last step.
-constexpr int kDB = 3, kNBB = 5, kR2B = 2, kBR = kR2B + 1, kR1B = 4, kRRB = 4, kPFB = 12;
+constexpr int kDB = 3, kNBB = 5, kR2B = 2, kBR = 4, kR1B = 4, kRRB = 4, kPFB = 12;   // kBR: 2 helpers x 2 blocks of b
 __host__ __device__ constexpr int ub_of(int WE) { return WE <= 4 ? 4 : 2; }   // steps per helper block
 template <typename T, bool UNIT, int WE>
-__global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
+__global__ void __launch_bounds__(384, 1) k_block(const BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
     constexpr int SH = kSH, UB = ub_of(WE), DB = kDB, NBB = kNBB, R2B = kR2B, R1B = kR1B, RRB = kRRB;
@@ -548,9 +548,10 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
     constexpr size_t TILE = ((size_t)NBB * UB * REC + (size_t)RRB * UB * 128 + (size_t)NCS * 32 * ES +
                              (size_t)kBR * UB * 32 * ES + 8 * (NBB + RRB) + 127) / 128 * 128;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ntw = blockDim.x >> 6;
+    const int ntw = blockDim.x / 96;              // tiles per CTA: 1 compute + 2 helper warps each
     const int w = warp % ntw;
     const bool helper = warp >= ntw;
+    const int hid = helper ? (warp - ntw) / ntw : 0;   // helper 0 takes even blocks, helper 1 odd
     unsigned char *tb = smem_raw + (size_t)w * TILE;
     unsigned char *ring = tb;                                        // [NBB*UB][REC]
     int32_t *rw = reinterpret_cast<int32_t *>(tb + (size_t)NBB * UB * REC);      // [RRB*UB][32]
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
     T *x = static_cast<T *>(a.x);
 
     for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
-    if (helper) {
+    if (helper && hid == 0) {
         for (int i = lane; i < NCS * 32; i += 32) cr[i] = Sentinel<T>::value();
         if (lane == 0) {
             for (int i = 0; i < NBB + RRB; ++i) mbar_init(&recbar[i], 1);
@@ -586,13 +587,15 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
         const int nblk = (n + UB - 1) / UB;
         const unsigned char *grec = a.recs + (size_t)s0 * REC;
         const int32_t *grow = a.rows + (size_t)s0 * 32;
-        const bool trace = g_trace != nullptr;
-        // lane 0: TMA of record block kk into ring block slot, row-id block kk into its slot
-        auto issue_rec = [&](int kk, int slot) {
+        const bool trace = g_trace != nullptr && hid == 0;
+        T *bh = br + hid * 2 * UB * 32;          // this helper's b ring: its blocks k (slot) and k+2
+        auto issue_rec = [&](int kk) {          // lane 0: TMA of record block kk
+            const int slot = kk % NBB;
             mbar_arrive_expect_tx(&recbar[slot], UB * REC);
             bulk_g2s(ring + (size_t)slot * UB * REC, grec + (size_t)kk * UB * REC, UB * REC, &recbar[slot]);
         };
-        auto issue_rows = [&](int kk, int slot) {
+        auto issue_rows = [&](int kk) {
+            const int slot = kk % RRB;
             mbar_arrive_expect_tx(&rowbar[slot], UB * 128);
             bulk_g2s(rw + slot * UB * 32, grow + (size_t)kk * UB * 32, UB * 128, &rowbar[slot]);
         };
@@ -600,19 +603,21 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grec + (size_t)kk * UB * REC), "r"(UB * REC)
                          : "memory");
         };
-        auto issue_b = [&](int rslot, int bslot) {       // b of one block, rows from row-ring slot rslot
-            const int32_t *rr = rw + rslot * UB * 32 + lane;
-            T *bb = br + bslot * UB * 32 + lane;
+        auto rec_wait = [&](int kk) { mbar_wait_wd(&recbar[kk % NBB], (uint32_t)((kk / NBB) & 1)); };
+        auto issue_b = [&](int kk, int bslot) {  // b of block kk (row ids landed)
+            mbar_wait_wd(&rowbar[kk % RRB], (uint32_t)((kk / RRB) & 1));
+            const int32_t *rr = rw + (kk % RRB) * UB * 32 + lane;
+            T *bb = bh + bslot * UB * 32 + lane;
 #pragma unroll
             for (int j = 0; j < UB; ++j) {
                 const int r = rr[j * 32];
                 cp_async_val_if(bb + j * 32, b + r, r >= 0);
             }
         };
-        // EXT values of one block: loaded one block ahead (an L2 round trip of slack)
         int32_t ncode[UB][WE];
         T nv[UB][WE];
-        auto ext_loads = [&](const unsigned char *rb, int kk) {
+        auto ext_loads = [&](int kk) {           // EXT values of block kk (records landed)
+            const unsigned char *rb = ring + (size_t)(kk % NBB) * UB * REC;
 #pragma unroll
             for (int j = 0; j < UB; ++j) {
                 const int32_t *ec = reinterpret_cast<const int32_t *>(rb + j * REC + ECO) + lane;
@@ -627,38 +632,26 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
                 }
             }
         };
-        if (lane == 0) {
+        if (hid == 0 && lane == 0) {
             for (int kk = 0; kk < min(nblk, kPFB); ++kk) prefetch_l2(kk);
-            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk, kk);
-            for (int kk = 0; kk < min(nblk, R1B); ++kk) issue_rows(kk, kk);
+            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk);
+            for (int kk = 0; kk < min(nblk, R1B); ++kk) issue_rows(kk);
         }
-        // b of blocks 0 .. R2B-1 (one cp.async group each)
-#pragma unroll 1
-        for (int kk = 0; kk < R2B; ++kk) {
-            if (kk < nblk) {
-                mbar_wait_wd(&rowbar[kk], 0u);
-                issue_b(kk, kk);
-            }
+        if (hid < nblk) {
+            issue_b(hid, 0);
             cp_async_commit();
+            rec_wait(hid);
+            __syncwarp();
+            ext_loads(hid);
         }
-        mbar_wait_wd(&recbar[0], 0u);
-        __syncwarp();
-        ext_loads(ring, 0);
-        // ring positions (blocks) and mbarrier phases, kept incrementally
-        int rs = 0, rsph = 0;                 // record slot of block k, its phase
-        int rd = DB % NBB;                    // record slot of block k+DB
-        int ro = R1B % RRB;                   // row slot of block k+R1B
-        int rq = R2B % RRB, rqph = (R2B / RRB) & 1;   // row slot / phase of block k+R2B
-        int bs = 0, bw = R2B % kBR;           // b block slot of block k / of block k+R2B
-        int cs = 0;                           // c slot (steps) of the block's first step
-        int cf = (DB * UB + UB - 1) % NCS;    // c slot of the last step of block k+DB-NBB
 #pragma unroll 1
-        for (int k = 0; k < nblk; ++k) {
+        for (int k = hid, i = 0; k < nblk; k += 2, ++i) {
             if (trace && lane == 0 && k * UB < g_trace_cap - 1) g_trace[(size_t)u * g_trace_cap + k * UB] = wd_now();
-            // (1) refill: records k+DB (its slot must be released by the compute warp), rows k+R1B
+            // (1) refill: records k+DB (the slot of block k+DB-NBB, released by the
+            // compute warp), rows k+R1B, L2 prefetch
             if (k + DB < nblk) {
                 if (k + DB >= NBB) {
-                    const T *f = cr + cf * 32 + lane;
+                    const T *f = cr + (((k + DB - NBB) * UB + UB - 1) % NCS) * 32 + lane;
                     if (__any_sync(0xffffffffu, !Sentinel<T>::is(lds_volatile(f)))) {
                         const unsigned long long t0 = wd_now();
                         unsigned it = 0;
@@ -668,23 +661,20 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
                         }
                     }
                 }
-                if (lane == 0) issue_rec(k + DB, rd);
+                if (lane == 0) issue_rec(k + DB);
             }
             if (lane == 0) {
-                if (k + R1B < nblk) issue_rows(k + R1B, ro);
+                if (k + R1B < nblk) issue_rows(k + R1B);
                 if (k + kPFB < nblk) prefetch_l2(k + kPFB);
             }
-            // (2) b of block k+R2B (row ids landed: mbarrier)
-            if (k + R2B < nblk) {
-                mbar_wait_wd(&rowbar[rq], (uint32_t)rqph);
-                issue_b(rq, bw);
-            }
+            // (2) b of this helper's next block k+2
+            if (k + 2 < nblk) issue_b(k + 2, (i + 1) & 1);
             cp_async_commit();
-            // (3) block k: records (mbarrier) and b (cp.async group k)
-            cp_async_wait<R2B>();
-            mbar_wait_wd(&recbar[rs], (uint32_t)rsph);
+            // (3) block k: b (this helper's previous group) and records
+            cp_async_wait<1>();
+            rec_wait(k);
             __syncwarp();
-            const unsigned char *rb = ring + (size_t)rs * UB * REC;
+            const unsigned char *rb = ring + (size_t)(k % NBB) * UB * REC;
             int32_t code[UB][WE];
             T v[UB][WE];
 #pragma unroll
@@ -694,12 +684,14 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
                     code[j][q] = ncode[j][q];
                     v[j][q] = nv[j][q];
                 }
-            // (4) EXT loads of block k+1
-            if (k + 1 < nblk) {
-                const int rs1 = rs + 1 == NBB ? 0 : rs + 1;
-                mbar_wait_wd(&recbar[rs1], (uint32_t)(rs1 == 0 ? rsph ^ 1 : rsph));
-                ext_loads(ring + (size_t)rs1 * UB * REC, k + 1);
+            // (4) EXT loads of this helper's next block k+2 (two blocks of slack)
+            if (k + 2 < nblk) {
+                rec_wait(k + 2);
+                __syncwarp();
+                ext_loads(k + 2);
             }
+            const int cs = (k * UB) % NCS;
+            const int bs = i & 1;
             // (5) block k's c values.  Fast path (every EXT value arrived, no
             // overflow row): straight-line over the UB steps.  Otherwise one step
             // at a time, publishing each c as soon as its values are there (a
@@ -716,7 +708,7 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
             if (!__any_sync(0xffffffffu, pend || ovf)) {
 #pragma unroll
                 for (int j = 0; j < UB; ++j) {
-                    T c = br[(bs * UB + j) * 32 + lane];
+                    T c = bh[(bs * UB + j) * 32 + lane];
 #pragma unroll
                     for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
                     sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
@@ -748,7 +740,7 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
                             if ((++it & 255u) == 0 && wd_expired(t0)) break;
                         } while (__any_sync(0xffffffffu, pj));
                     }
-                    T c = br[(bs * UB + j) * 32 + lane];
+                    T c = bh[(bs * UB + j) * 32 + lane];
 #pragma unroll
                     for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
                     if (((unsigned)code[j][0] & 0xE0000000u) == 0xE0000000u) {          // overflow list
@@ -770,16 +762,6 @@ __global__ void __launch_bounds__(256, 1) k_block(const BlockArgs a) {
                     sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
                 }
             }
-            if (++rs == NBB) { rs = 0; rsph ^= 1; }
-            if (++rd == NBB) rd = 0;
-            if (++ro == RRB) ro = 0;
-            if (++rq == RRB) { rq = 0; rqph ^= 1; }
-            if (++bs == kBR) bs = 0;
-            if (++bw == kBR) bw = 0;
-            cs += UB;
-            if (cs == NCS) cs = 0;
-            cf += UB;
-            if (cf >= NCS) cf -= NCS;
         }
         cp_async_wait<0>();
     } else if (n > 0) {
@@ -1210,11 +1192,11 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     const size_t smem = fixed_bytes() + (size_t)max_slots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 64 * wpc, smem));
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 96 * wpc, smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = 64 * wpc;
+    B.threads = 96 * wpc;
     B.nst = kNBB * ub_of(WE);
     B.bb = kR2B * ub_of(WE);
     B.d = kDB * ub_of(WE);
