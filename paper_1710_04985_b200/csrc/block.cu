@@ -764,6 +764,7 @@ __global__ void __launch_bounds__(384, 1) k_block(const BlockArgs a) {
             }
         }
         cp_async_wait<0>();
+        if (trace && lane == 0) g_trace[(size_t)u * g_trace_cap + g_trace_cap - 1] = wd_now();
     } else if (n > 0) {
         // software-pipelined: the next step's c and record fields are loaded
         // before this step's shuffle -> FMA chain; the readiness check of the
@@ -840,6 +841,311 @@ __global__ void __launch_bounds__(384, 1) k_block(const BlockArgs a) {
             atomicAdd(&a.ctr[0], 1u);
         }
     }
+}
+
+// ---------------------------------------------------------------- lean BLOCK
+// k_block1: the same records, ONE warp per tile doing everything (no helper
+// warp, no c hand-off between warps).  Per step t the warp
+//   (1) loads step t+1's record fields and its SMEM EXT values (shared slots
+//       written by other warps of the CTA, value-as-flag),
+//   (2) solves step t: readiness vote, c = b - sum_EXT a x (storage order),
+//       the SHFL chain, x * invd, stores,
+//   (3) issues step t+2's b[row] and GLOB EXT loads (relaxed) into registers:
+//       two steps of cover for an L2 round trip, so a consumer tile needs to
+//       lag its producer by only ~2 levels (a whole-block prefetch forced
+//       4-7 levels per CTA crossing, tools/wave_trace.py).
+// Per block of kLUB steps: record block k+kLDB by TMA (lane 0), L2 prefetch
+// of records kLPF blocks ahead and of b[row] of block k+2 (records landed).
+// A value still holding the sentinel is re-polled with two loads in flight
+// (half the round trip of overshoot instead of a whole one).  Arithmetic
+// order equals k_block's (bitwise-equal x).
+constexpr int kLUB = 4, kLDB = 3, kLNBB = kLDB + 2, kLPF = 12, kLPB = 4;
+__host__ __device__ constexpr size_t lean_tile_bytes_c(int REC, int) {
+    return ((size_t)kLNBB * kLUB * REC + 8 * kLNBB + 127) / 128 * 128;
+}
+
+template <typename T, int WE>
+struct LState {
+    int4 ci;
+    CV<T> cv;
+    int32_t code[WE];
+    T ev[WE];
+    T v[WE];              // SMEM EXT values (0 for other kinds)
+};
+
+// overflow list of one row (rows with more EXT terms than WE): slow path
+template <typename T>
+__device__ __noinline__ T lean_ovf(T c, int o, const int32_t *__restrict__ ovf_code, const T *__restrict__ ovf_val,
+                                   const T *slots, const T *gm) {
+    for (;; ++o) {
+        const int32_t cc = ovf_code[o];
+        if (cc == kNone) break;
+        T vv;
+        if (code_kind(cc) == 1u) {
+            vv = lds_volatile(slots + code_idx(cc));
+            if (Sentinel<T>::is(vv)) vv = poll_smem_slow(slots + code_idx(cc));
+        } else {
+            vv = ld_relaxed_val(gm + code_idx(cc));
+            if (Sentinel<T>::is(vv)) vv = poll_global_slow(gm + code_idx(cc));
+        }
+        c = fnma(ovf_val[o], vv, c);
+    }
+    return c;
+}
+
+__device__ __forceinline__ double ldg_nc_if(const double *p, bool pred) {
+    double v = 0.0;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.f64 %0, [%1];\n\t}"
+                 : "+d"(v) : "l"(p), "r"((unsigned)pred));
+    return v;
+}
+__device__ __forceinline__ float ldg_nc_if(const float *p, bool pred) {
+    float v = 0.f;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.f32 %0, [%1];\n\t}"
+                 : "+f"(v) : "l"(p), "r"((unsigned)pred));
+    return v;
+}
+__device__ __forceinline__ void prefetch_l2_if(const void *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q prefetch.global.L2 [%0];\n\t}" ::"l"(p),
+                 "r"((unsigned)pred));
+}
+
+template <typename T, bool UNIT, int WE>
+__global__ void __launch_bounds__(128, 1) k_block1(const BlockArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ unsigned s_epoch;
+    constexpr int SH = kSH, UB = kLUB, DB = kLDB, NBB = kLNBB;
+    constexpr int ES = (int)sizeof(T);
+    constexpr int REC = rec_bytes(SH, WE, ES);
+    constexpr int CVO = rec_cv(SH), ECO = rec_ec(SH, ES), EVO = rec_ev(SH, WE, ES);
+    constexpr size_t TILE = lean_tile_bytes_c(REC, ES);
+    static_assert(UB % 2 == 0 && UB >= 2, "ping-pong state needs an even block length");
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ntw = blockDim.x >> 5;
+    unsigned char *tb = smem_raw + (size_t)w * TILE;
+    unsigned char *ring = tb;                                                       // [NBB][UB][REC]
+    uint64_t *recbar = reinterpret_cast<uint64_t *>(tb + (size_t)NBB * UB * REC);
+    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)ntw * TILE);
+    const T *b = static_cast<const T *>(a.b);
+    T *x = static_cast<T *>(a.x);
+
+    for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
+    if (lane == 0) {
+        for (int i = 0; i < NBB; ++i) mbar_init(&recbar[i], 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x == 0) s_epoch = (unsigned)ld_relaxed(reinterpret_cast<const int *>(a.ctr));
+    __syncthreads();
+    const unsigned par = s_epoch & 1u;
+    T *gm = static_cast<T *>(a.gmb) + (size_t)par * a.G;
+    {   // re-arm this CTA's mailboxes of the idle array (written by the previous solve)
+        T *go = static_cast<T *>(a.gmb) + (size_t)(par ^ 1u) * a.G;
+        for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
+            go[i] = Sentinel<T>::value();
+    }
+
+    const int u = blockIdx.x * ntw + w;
+    const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;
+    if (n > 0) {
+        const int nblk = (n + UB - 1) / UB;
+        const unsigned char *grec = a.recs + (size_t)s0 * REC;
+        unsigned long long *trc = g_trace != nullptr ? g_trace + (size_t)u * g_trace_cap : nullptr;
+        long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // debug trace only (g_trace set): cycle counters
+        auto issue_rec = [&](int kk) {
+            const int slot = kk % NBB;
+            mbar_arrive_expect_tx(&recbar[slot], UB * REC);
+            bulk_g2s(ring + (size_t)slot * UB * REC, grec + (size_t)kk * UB * REC, UB * REC, &recbar[slot]);
+        };
+        auto prefetch_rec = [&](int kk) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grec + (size_t)kk * UB * REC), "r"(UB * REC)
+                         : "memory");
+        };
+        auto rec_wait = [&](int kk) { mbar_wait_wd(&recbar[kk % NBB], (uint32_t)((kk / NBB) & 1)); };
+        // b[row] is L2-prefetched kLPB-1 blocks ahead from row ids loaded one block earlier
+        const int32_t *grow = a.rows + (size_t)s0 * 32 + lane;
+        int32_t rowreg[UB];
+        auto load_rows = [&](int kk) {
+#pragma unroll
+            for (int j = 0; j < UB; ++j) rowreg[j] = kk < nblk ? __ldg(grow + ((size_t)kk * UB + j) * 32) : -1;
+        };
+        auto prefetch_b = [&]() {
+#pragma unroll
+            for (int j = 0; j < UB; ++j) prefetch_l2_if(b + rowreg[j], rowreg[j] >= 0);
+        };
+        // start of block kb: refill the record ring, b prefetch
+        auto block_work = [&](int kb) {
+            const long long c0 = trc != nullptr ? clock64() : 0;
+            __syncwarp();
+            if (lane == 0) {
+                if (kb + DB < nblk) issue_rec(kb + DB);
+                if (kb + kLPF < nblk) prefetch_rec(kb + kLPF);
+            }
+            prefetch_b();                        // b of block kb + kLPB - 1
+            load_rows(kb + kLPB);
+            if (kb + 1 < nblk) rec_wait(kb + 1);
+            if (trc != nullptr) dbg[4] += clock64() - c0;
+        };
+        auto load_state = [&](LState<T, WE> &S, const unsigned char *r) {
+            S.ci = reinterpret_cast<const int4 *>(r)[lane];
+            S.cv.load(r + CVO, lane);
+#pragma unroll
+            for (int q = 0; q < WE; ++q) {
+                S.code[q] = reinterpret_cast<const int32_t *>(r + ECO)[q * 32 + lane];
+                S.ev[q] = reinterpret_cast<const T *>(r + EVO)[q * 32 + lane];
+                S.v[q] = lds_flag_if(slots + code_idx(S.code[q]), code_kind(S.code[q]) == 1u);
+            }
+        };
+        // b and GLOB EXT values of a step, loads in flight until first use
+        T Bv[2], Gv[2][WE];
+        auto issue_far = [&](int par2, const unsigned char *r, bool valid) {
+            const int row = reinterpret_cast<const int4 *>(r)[lane].x;
+            Bv[par2] = ldg_nc_if(b + row, valid && row >= 0);
+#pragma unroll
+            for (int q = 0; q < WE; ++q) {
+                const int32_t cd = reinterpret_cast<const int32_t *>(r + ECO)[q * 32 + lane];
+                Gv[par2][q] = ldg_flag_if(gm + code_idx(cd), valid && code_kind(cd) == 2u);
+            }
+        };
+
+        if (lane == 0) {
+            for (int kk = 0; kk < min(nblk, kLPF); ++kk) prefetch_rec(kk);
+            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk);
+        }
+        for (int kk = 0; kk < kLPB - 1; ++kk) {
+            load_rows(kk);
+            prefetch_b();
+        }
+        load_rows(kLPB - 1);
+        rec_wait(0);
+        issue_far(0, ring, true);
+        issue_far(1, ring + REC, n > 1);
+        block_work(0);
+
+        LState<T, WE> st[2];
+        load_state(st[0], ring);
+        T xprev = T(0);
+        int rslot = 0;
+        // one block of UB steps; false when the warp's steps are done
+        auto do_block = [&](int k) -> bool {
+            if (trc != nullptr && lane == 0 && k * UB < g_trace_cap - 16) trc[k * UB] = wd_now();
+            const unsigned char *rbk = ring + (size_t)rslot * UB * REC;
+            const int rslot1 = rslot + 1 == NBB ? 0 : rslot + 1;
+            const unsigned char *rbk1 = ring + (size_t)rslot1 * UB * REC;
+#pragma unroll
+            for (int j = 0; j < UB; ++j) {
+                const int t = k * UB + j;
+                if (t >= n) return false;
+                LState<T, WE> &S = st[j & 1];
+                LState<T, WE> &N = st[(j + 1) & 1];
+                const bool more = t + 1 < n;
+                if (more) {
+                    if (j == UB - 1) {
+                        block_work(k + 1);
+                        load_state(N, rbk1);
+                    } else {
+                        load_state(N, rbk + (size_t)(j + 1) * REC);
+                    }
+                }
+                // EXT readiness (value-as-flag); slow path re-polls with two loads in flight
+                T v[WE];
+                bool pend = false;
+#pragma unroll
+                for (int q = 0; q < WE; ++q) {
+                    const unsigned kind = code_kind(S.code[q]);
+                    v[q] = kind == 2u ? Gv[j & 1][q] : S.v[q];
+                    pend |= (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
+                }
+                if (__any_sync(0xffffffffu, pend)) {
+                    const unsigned long long t0 = wd_now();
+                    const long long c0 = trc != nullptr ? clock64() : 0;
+                    unsigned it = 0;
+                    T inf[WE];
+                    auto issue_polls = [&](T (&dst)[WE]) {
+#pragma unroll
+                        for (int q = 0; q < WE; ++q) {
+                            const unsigned kind = code_kind(S.code[q]);
+                            const bool p = (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
+                            const T vs_ = lds_flag_if(slots + code_idx(S.code[q]), p && kind == 1u);
+                            const T vg_ = ldg_flag_if(gm + code_idx(S.code[q]), p && kind == 2u);
+                            dst[q] = kind == 1u ? vs_ : vg_;
+                        }
+                    };
+                    issue_polls(inf);
+                    do {
+                        T nx[WE];
+                        __nanosleep(32);
+                        issue_polls(nx);
+                        pend = false;
+#pragma unroll
+                        for (int q = 0; q < WE; ++q) {
+                            const unsigned kind = code_kind(S.code[q]);
+                            const bool p = (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
+                            v[q] = (p && !Sentinel<T>::is(inf[q])) ? inf[q] : v[q];
+                            pend |= (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
+                            inf[q] = nx[q];
+                        }
+                        if ((++it & 255u) == 0 && wd_expired(t0)) break;
+                    } while (__any_sync(0xffffffffu, pend));
+                    if (trc != nullptr) {
+                        bool gl = false;
+#pragma unroll
+                        for (int q = 0; q < WE; ++q) gl |= code_kind(S.code[q]) == 2u;
+                        gl = __any_sync(0xffffffffu, gl);
+                        if (t == 0) dbg[0] += clock64() - c0;
+                        else if (gl) { dbg[1] += clock64() - c0; ++dbg[2]; }
+                        else { dbg[3] += clock64() - c0; ++dbg[7]; }
+                    }
+                }
+                T c = Bv[j & 1];
+#pragma unroll
+                for (int q = 0; q < WE; ++q) c = fnma(S.ev[q], v[q], c);
+                if (((unsigned)S.code[0] & 0xE0000000u) == 0xE0000000u && S.ci.x >= 0)
+                    c = lean_ovf<T>(c, S.code[0] & 0x1FFFFFFF, a.ovf_code, static_cast<const T *>(a.ovf_val), slots,
+                                    gm);
+                const int nsh = S.ci.w & 7;
+                T acc = Sentinel<T>::scrub(c);
+#pragma unroll
+                for (int q = 0; q < SH; ++q) {
+                    const T vq = __shfl_sync(0xffffffffu, xprev, (S.ci.w >> (3 + 5 * q)) & 31);
+                    acc = fnma(S.cv.v[1 + q], q < nsh ? vq : T(0), acc);
+                }
+                const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S.cv.v[0];
+                if (S.ci.x >= 0) __stcg(x + S.ci.x, xi);
+                if (S.ci.y >= 0) sts_flag(slots + S.ci.y, xi);
+                if (S.ci.z >= 0) stg_flag(gm + S.ci.z, xi);
+                xprev = xi;
+                // (3) step t+2's b and GLOB loads (its records have landed)
+                if (j + 2 < UB) issue_far(j & 1, rbk + (size_t)(j + 2) * REC, t + 2 < n);
+                else issue_far(j & 1, rbk1 + (size_t)(j + 2 - UB) * REC, t + 2 < n);
+            }
+            rslot = rslot1;
+            return true;
+        };
+#pragma unroll 1
+        for (int k = 0; k < nblk; ++k)
+            if (!do_block(k)) break;
+        if (trc != nullptr && lane == 0) {
+            trc[g_trace_cap - 1] = wd_now();
+            for (int i = 0; i < 8; ++i) trc[g_trace_cap - 16 + i] = (unsigned long long)dbg[i];
+        }
+    }
+
+    __syncthreads();
+    if (threadIdx.x == 0) {      // the last CTA to finish advances the mailbox epoch
+        __threadfence();
+        if (atomicAdd(&a.ctr[1], 1u) == gridDim.x - 1) {
+            atomicExch(&a.ctr[1], 0u);
+            __threadfence();
+            atomicAdd(&a.ctr[0], 1u);
+        }
+    }
+}
+
+template <typename T, bool UNIT>
+void *pick_kernel_lean(int W, int &we) {
+    if (W <= 3) { we = 2; return (void *)k_block1<T, UNIT, 2>; }
+    we = 4;
+    return (void *)k_block1<T, UNIT, 4>;
 }
 
 // per-tile shared memory of k_block (must match TILE there)
@@ -974,10 +1280,22 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(W, WE) : pick_kernel<double, false>(W, WE);
     else
         kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(W, WE) : pick_kernel<float, false>(W, WE);
+    // lean kernel (one warp per tile, k_block1) when SPTRSV_BLOCK_LEAN=1 (opt-in:
+    // cfg2 0.327 ms vs 0.271 ms for the helper design, profiles/lean_block_r1f.md);
+    // rows with more than 4 EXT terms use the overflow lists
+    const bool lean = env_int("SPTRSV_BLOCK_LEAN", 0) != 0;
+    if (lean) {
+        if (h->dtype == SPTRSV_F64)
+            kn = h->diag == SPTRSV_UNIT ? pick_kernel_lean<double, true>(W, WE) : pick_kernel_lean<double, false>(W, WE);
+        else
+            kn = h->diag == SPTRSV_UNIT ? pick_kernel_lean<float, true>(W, WE) : pick_kernel_lean<float, false>(W, WE);
+    }
     const int REC = rec_bytes(kSH, WE, (int)es);
     const size_t budget = (size_t)max_smem - 1024;          // static smem + slack
     // per CTA (nt tiles): the tiles' rings; the rest holds shared slots
-    auto ring_bytes = [&](int nt) { return (size_t)nt * block_tile_bytes(REC, (int)es, ub_of(WE)); };
+    auto ring_bytes = [&](int nt) {
+        return (size_t)nt * (lean ? lean_tile_bytes_c(REC, (int)es) : block_tile_bytes(REC, (int)es, ub_of(WE)));
+    };
 
     // ---- 2. partition rows over U = K x wpc warps of K co-resident CTAs
     int32_t *unit = nullptr;
@@ -1192,14 +1510,16 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     const size_t smem = fixed_bytes() + (size_t)max_slots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 96 * wpc, smem));
+    const int tpw = lean ? 32 : 96;          // threads per tile
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, tpw * wpc, smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = 96 * wpc;
-    B.nst = kNBB * ub_of(WE);
-    B.bb = kR2B * ub_of(WE);
-    B.d = kDB * ub_of(WE);
+    B.threads = tpw * wpc;
+    B.lean = lean;
+    B.nst = lean ? kLNBB * kLUB : kNBB * ub_of(WE);
+    B.bb = lean ? 2 : kR2B * ub_of(WE);
+    B.d = lean ? kLDB * kLUB : kDB * ub_of(WE);
     B.W = WE;
     B.rec_bytes = REC;
     B.nent = (int64_t)nsteps * REC;

@@ -33,6 +33,7 @@ struct DevArena {
 // Block-schedule (SPTRSV_ALGO_BLOCK) device data; see block.cu.
 struct BlockPlan {
     bool built = false;
+    bool lean = false;        // k_block1 (one warp per tile) instead of k_block
     int32_t nblocks = 0;      // K co-resident CTAs
     int32_t wpc = 0;          // tiles per CTA
     int32_t nunits = 0;       // K x wpc tiles (a compute and a helper warp each)

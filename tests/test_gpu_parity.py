@@ -376,3 +376,46 @@ def test_tile_not_supported_off_grid(S):
         S.from_csr(m, algo="tile")
     sv = S.from_csr(m, algo="auto")                  # auto falls back to SELF off grids
     assert sv.info()["algo"] == 0
+
+
+# ------------------------------------------------------------ lean BLOCK (k_block1, SPTRSV_BLOCK_LEAN=1)
+LEAN_CASES = TILE_CASES + [((96, 96, 96), 27, "lower")]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("dims,pts,uplo", LEAN_CASES)
+def test_lean_block_grids(S, dims, pts, uplo, dtype, monkeypatch):
+    """The one-warp-per-tile kernel: oracle tolerance, run-to-run bitwise, and
+    bitwise equal to the helper kernel (same records, same arithmetic order).
+    27-point rows have more EXT terms than its 4 record entries: overflow lists."""
+    m = workloads.stencil(dims, pts, uplo)
+    b = workloads.rhs(m.n, 1, seed=len(dims) * 10 + pts + 1)[:, 0]
+    ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, dtype=dtype)
+    x0, _ = gpu_solve(S, m, b, uplo, dtype=dtype, algo="block")
+    monkeypatch.setenv("SPTRSV_BLOCK_LEAN", "1")
+    x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="block")
+    assert relerr(x, ref) <= TOL[dtype]
+    assert np.array_equal(x, x0)
+    x2, _ = gpu_solve(S, m, b, dtype=dtype, solver=sv)
+    assert np.array_equal(x, x2)
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("uplo,diag", [("lower", "non_unit"), ("upper", "unit")])
+def test_lean_block_random_and_integer(S, seed, uplo, diag, monkeypatch):
+    """Natural-order partition (no grid): SMEM/GLOB/overflow EXT terms of every kind."""
+    monkeypatch.setenv("SPTRSV_BLOCK_LEAN", "1")
+    m = random_triangular_fast(2500 + 611 * seed, 3.0 + seed, seed, uplo)
+    b = workloads.rhs(m.n, 1, seed=seed)[:, 0]
+    ref = oracle.solve(m, b, uplo, diag)
+    x, _ = gpu_solve(S, m, b, uplo, diag, algo="block")
+    assert relerr(x, ref) <= 1e-10
+    g = workloads.stencil((40, 30, 20), 7, uplo, diag=8.0)
+    xt = workloads.integer_xtrue(g.n, 1, seed=101 + seed)[:, 0]
+    bb = oracle.matvec(g, xt, uplo)
+    xg, sv = gpu_solve(S, g, bb, uplo, algo="block")
+    assert np.array_equal(xg, xt)
+    bt = torch.from_numpy(bb).cuda()                    # in place
+    sv.solve(bt, x=bt)
+    torch.cuda.synchronize()
+    assert np.array_equal(bt.cpu().numpy(), xt)
