@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "tile", "auto"],
+    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "tile", "slfc", "levc", "auto"],
                     help="auto: BLOCK when the analysis detects a structured grid, else SELF")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -93,17 +93,18 @@ def work_counts(m, solves, nrhs, esize):
     return sum(p[0] for p in per), sum(p[1] for p in per)
 
 
-ALGO_NAMES = {0: "self", 1: "level", 2: "block", 4: "tile"}
+ALGO_NAMES = {0: "self", 1: "level", 2: "block", 4: "tile", 5: "slfc", 6: "levc"}
 
 
 def kernel_of(info, nrhs):
     """(dominant kernel, launches per solve) of a handle's solve path."""
     algo = ALGO_NAMES.get(info["algo"], "self")
     if nrhs == 1:
-        return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1), "tile": ("k_tile", 1)}[algo]
+        return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1), "tile": ("k_tile", 1),
+                "slfc": ("k_slfc", 1), "levc": ("k_levc", 1)}[algo]
     if algo in ("block", "tile") and os.environ.get("SPTRSV_MRHS_TILE") == "1":
         return ("k_tile_mrhs", 1)
-    return ("k_mrhs", 1) if algo == "self" else ("k_level_mrhs", 1)
+    return ("k_mrhs", 1) if algo in ("self", "slfc") else ("k_level_mrhs", 1)
 
 
 def measured_peak():
@@ -354,7 +355,7 @@ def run_ours(args):
     # extra: the other algorithms on the same problem (context, rank 0 prints)
     extra = {}
     if args.extra and world == 1:
-        for algo in ("self", "level", "block", "tile"):
+        for algo in ("self", "level", "block", "tile", "slfc", "levc"):
             if algo == args.algo:
                 continue
             try:

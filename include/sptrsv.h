@@ -60,9 +60,16 @@ typedef enum {
                                hand-offs (any matrix, fastest on structured grids) */
     SPTRSV_ALGO_AUTO = 3,   /* BLOCK when the analysis detects a structured grid, else SELF;
                                info.algo then reports the algorithm chosen */
-    SPTRSV_ALGO_TILE = 4    /* CTA tiles: level-synchronous inside a CTA (x in shared memory),
+    SPTRSV_ALGO_TILE = 4,   /* CTA tiles: level-synchronous inside a CTA (x in shared memory),
                                producer-CTA level counters between CTAs;
                                structured grids with <= 3 dependencies per row */
+    SPTRSV_ALGO_SLFC = 5,   /* column-wise self-scheduled (Alg. SLFC, kernel P:631-653):
+                               per-column dependency counters, x updates pushed by L2
+                               atomics; last-bit results vary run to run (atomic order).
+                               nrhs > 1 solves use the self-scheduled row kernel */
+    SPTRSV_ALGO_LEVC = 6    /* column-wise level-scheduled (Alg. LEVC, kernel
+                               P:536-552): atomics, grid-wide barrier per level.  nrhs > 1
+                               solves use the level-scheduled row kernel */
 } sptrsv_algo_t;
 
 typedef enum {

@@ -58,6 +58,8 @@ def _load():
             f = getattr(lib, name)
             f.restype = ctypes.c_int
             f.argtypes = [i32, vp, vp, vp, ctypes.c_int, ctypes.c_int, i32, vp, vp]
+        lib.oracle_solve_col_f64.restype = ctypes.c_int
+        lib.oracle_solve_col_f64.argtypes = [i32, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp]
         lib.oracle_kahn.restype = i32
         lib.oracle_kahn.argtypes = [i32, vp, vp, ctypes.c_int, vp, vp, vp]
         lib.oracle_backward_error.restype = ctypes.c_double
@@ -153,6 +155,20 @@ def solve(m, b, uplo="lower", diag="non_unit", dtype=np.float64):
     if st != 0:
         raise OracleError(STATUS[st])
     return x.reshape(-1) if squeeze else x
+
+
+def solve_col(m, b, uplo="lower", diag="non_unit"):
+    """Column-wise sweep over the CSC of the referenced strict
+    triangle: x := f; x(i) /= d(i); x(jb) -= b x(i).  One fp64 RHS."""
+    rowptr, colidx = _csr(m)
+    f = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(-1))
+    x = np.zeros_like(f)
+    vals = np.ascontiguousarray(m.vals, dtype=np.float64)
+    st = _load().oracle_solve_col_f64(m.n, _p(rowptr), _p(colidx), _p(vals), _UPLO[uplo], _DIAG[diag],
+                                      _p(f), _p(x))
+    if st != 0:
+        raise OracleError(STATUS[st])
+    return x
 
 
 def pair_solve(m, b, dtype=np.float64):

@@ -20,6 +20,7 @@
  *   oracle_schedule   O-4      nlev, ilev, jlev (stable)
  *   oracle_solve_f64  O-5      row-wise substitution
  *   oracle_solve_f32  O-5      same, float storage + accumulation (REAL)
+ *   oracle_solve_col_f64       column-wise sweep over the CSC
  *   oracle_kahn       A18      Kahn topological sort by rounds
  *   oracle_backward_error      pin helper: componentwise backward error
  *
@@ -226,6 +227,52 @@ int oracle_solve_f64(int32_t n, const int32_t *rowptr, const int32_t *colidx, co
         }
     }
     free(diagk);
+    return OR_SUCCESS;
+}
+
+/*
+ * Column-wise sweep (Section "Column-wise SpTrSv"): x := f, then
+ * for i = 1..n (upper: n..1) x(i) := x(i)/d(i) and every entry b(j) of
+ * column i updates x(jb(j)) := x(jb(j)) - b(j)*x(i).  The CSC (ib, jb, b) of
+ * the referenced strict triangle is built here by counting, entries of a
+ * column in increasing row order.  The reference for the column-wise GPU
+ * solves (SLFC / LEVC); same result as O-5 up to rounding order.
+ */
+int oracle_solve_col_f64(int32_t n, const int32_t *rowptr, const int32_t *colidx, const double *vals,
+                         int uplo, int diag, const double *f, double *x) {
+    int32_t *diagk = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t *ib = (int32_t *)calloc((size_t)n + 1, sizeof(int32_t));
+    if (!diagk || !ib) { free(diagk); free(ib); return OR_ALLOC; }
+    int st = oracle_select(n, rowptr, colidx, vals, uplo, diag, NULL, diagk, NULL, NULL, NULL, NULL);
+    if (st != OR_SUCCESS) { free(diagk); free(ib); return st; }
+    for (int32_t r = 0; r < n; ++r)                       /* column counts */
+        for (int32_t k = rowptr[r]; k < rowptr[r + 1]; ++k)
+            if (in_triangle(r, colidx[k], uplo)) ib[colidx[k] + 1]++;
+    for (int32_t i = 0; i < n; ++i) ib[i + 1] += ib[i];
+    int32_t nnz = ib[n];
+    int32_t *jb = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nnz > 0 ? nnz : 1));
+    double *bv = (double *)malloc(sizeof(double) * (size_t)(nnz > 0 ? nnz : 1));
+    int32_t *fill = (int32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+    if (!jb || !bv || !fill) { free(diagk); free(ib); free(jb); free(bv); free(fill); return OR_ALLOC; }
+    for (int32_t r = 0; r < n; ++r)                       /* rows ascending: column entries by row */
+        for (int32_t k = rowptr[r]; k < rowptr[r + 1]; ++k) {
+            int32_t c = colidx[k];
+            if (in_triangle(r, c, uplo)) {
+                int32_t q = ib[c] + fill[c]++;
+                jb[q] = r;
+                bv[q] = vals[k];
+            }
+        }
+    for (int32_t i = 0; i < n; ++i) x[i] = f[i];          /* x := f */
+    for (int32_t t = 0; t < n; ++t) {
+        int32_t i = (uplo == OR_LOWER) ? t : n - 1 - t;
+        if (diag != OR_UNIT) x[i] = x[i] / vals[diagk[i]];
+        for (int32_t j = ib[i]; j < ib[i + 1]; ++j) {
+            double p = bv[j] * x[i];
+            x[jb[j]] = x[jb[j]] - p;
+        }
+    }
+    free(diagk); free(ib); free(jb); free(bv); free(fill);
     return OR_SUCCESS;
 }
 

@@ -146,7 +146,8 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
 extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
     if (!h) return SPTRSV_ERR_INVALID_VALUE;
     if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK &&
-        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_TILE)
+        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_TILE && algo != SPTRSV_ALGO_SLFC &&
+        algo != SPTRSV_ALGO_LEVC)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
     const bool want_block = algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_AUTO || algo == SPTRSV_ALGO_TILE;

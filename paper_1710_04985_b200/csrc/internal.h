@@ -124,6 +124,13 @@ struct sptrsv_handle_s {
     int32_t *d_mr_ptr = nullptr;
     int32_t *d_mr_col = nullptr;
     void *d_mr_val = nullptr;
+    // CSC of the referenced strict triangle (SLFC / LEVC, column.cu; built on first use)
+    bool csc_built = false;
+    int32_t *d_c_ptr = nullptr;              // [n+1] by column (row id)
+    int32_t *d_c_row = nullptr;              // dependent rows of each column
+    void *d_c_val = nullptr;
+    int32_t *d_count = nullptr;              // [n] SLFC dependency counters (reset from d_dp per solve)
+    int32_t slfc_grid = 0;
     // synchronisation state
     int32_t *d_flags = nullptr;              // [n] per-row ready flags (epoch tagged)
     int32_t epoch = 0;
@@ -131,6 +138,7 @@ struct sptrsv_handle_s {
     unsigned long long *d_bar = nullptr;     // level barrier counter (monotone)
     unsigned long long bar_base = 0;
     int32_t self_grid = 0, level_grid = 0, mrhs_grid = 0;
+    bool self_u16 = false;                   // k_self instance of self_grid (SPTRSV_WPR_U)
     // in-place / host staging
     void *d_stage = nullptr;
     size_t stage_bytes = 0;
@@ -149,6 +157,8 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
 sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t tile_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t tile_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
+sptrsv_status_t column_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);   // column.cu
+sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s);                            // solve.cu
 // device scans (analyze.cu)
 sptrsv_status_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
 sptrsv_status_t exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, DevArena &tmp, cudaStream_t s);

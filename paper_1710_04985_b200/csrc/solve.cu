@@ -31,6 +31,18 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// Debug hook (sptrsv_dbg_self_trace, not part of include/sptrsv.h): when set,
+// k_self writes %globaltimer at the publication of every row.
+__device__ unsigned long long *g_tpub = nullptr;
+__device__ __forceinline__ void trace_pub(int row) {
+    unsigned long long *p = g_tpub;
+    if (p != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p[row] = t;
+    }
+}
+
 template <typename T, bool UNIT>
 __device__ __forceinline__ T finish(T s, T di) { return UNIT ? s : s * di; }
 
@@ -53,6 +65,24 @@ __device__ __forceinline__ void wait_flags(const int *flags, const int (&cols)[N
             }
         }
     }
+}
+
+// Value-as-flag wait: re-load every pending value (relaxed, L2) after a short
+// sleep until none is the sentinel.  (A two-wave variant with reloads half a
+// round trip apart measured slower on cfg4: 38 vs 32 ms, the spinning warps
+// load the SMs and L2 more than the shorter overshoot saves.)
+template <typename T, int N>
+__device__ __forceinline__ bool pending_any(const int (&c)[N], const T (&v)[N]) {
+    bool pend = false;
+#pragma unroll
+    for (int u = 0; u < N; ++u) pend |= c[u] >= 0 && Sentinel<T>::is(v[u]);
+    return pend;
+}
+template <typename T, int N>
+__device__ __forceinline__ void reload_pending(const int (&c)[N], T (&v)[N], const T *x) {
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+        if (c[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + c[u]);
 }
 
 // ---------------------------------------------------------------- TPR row
@@ -92,19 +122,23 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
     if (WAIT) {
 #pragma unroll
         for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_relaxed_val(x + cols[k]) : T(0);
-        bool pend = false;
+        // each lane publishes its row as soon as ITS dependencies are there
+        // (not when the chunk's slowest lane is): a row's consumers never
+        // wait for an unrelated row of the same chunk
+        bool done = !act;
+        for (;;) {
+            if (!done && !pending_any<T, kTprMax>(cols, xv)) {
 #pragma unroll
-        for (int k = 0; k < kTprMax; ++k) pend |= (cols[k] >= 0) && Sentinel<T>::is(xv[k]);
-        while (pend) {
-            pend = false;
-            __nanosleep(20);
-#pragma unroll
-            for (int k = 0; k < kTprMax; ++k) {
-                if (cols[k] >= 0 && Sentinel<T>::is(xv[k])) {
-                    xv[k] = ld_relaxed_val(x + cols[k]);
-                    pend |= Sentinel<T>::is(xv[k]);
+                for (int k = 0; k < kTprMax; ++k) {
+                    if (cols[k] >= 0) s = fnma(vals[k], xv[k], s);
                 }
+                st_relaxed_val(x + row, Sentinel<T>::scrub(finish<T, UNIT>(s, di)));
+                trace_pub(row);
+                done = true;
             }
+            if (__all_sync(0xffffffffu, done)) return;
+            __nanosleep(20);
+            reload_pending<T, kTprMax>(cols, xv, x);
         }
     } else {
 #pragma unroll
@@ -122,38 +156,75 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
 }
 
 // ---------------------------------------------------------------- WPR row
-template <typename T, bool UNIT, bool WAIT>
+template <typename T, bool UNIT, bool WAIT, int U = 8>
 __device__ __forceinline__ void wpr_row(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                         const T *__restrict__ invd, const int32_t *__restrict__ ecol,
                                         const T *__restrict__ eval, const T *b, T *x) {
+    // Batches of 32 x U entries: every lane has U dependency loads in
+    // flight at once (one L2 round trip per batch instead of per 32 entries),
+    // and the next batch's indices/values are loaded before this batch is
+    // polled.  Per lane the entries are still accumulated k = lane, lane+32,
+    // ... in increasing order (bitwise equal to the one-at-a-time loop).
     const int width = chunk_width(cd.meta);
     const int row = perm[cd.pos];
     const int32_t *ec = ecol + cd.eptr;
     const T *ev = eval + cd.eptr;
+    // b(i) and 1/d(i) before the dependencies: not a DRAM round trip after the reduction
+    const T bi = lane == 0 ? ld_cg(b + row) : T(0);
+    const T di = lane == 0 ? invd[cd.pos] : T(0);
     T acc = T(0);
-    for (int k = lane; k < width; k += 32) {
-        const int c = ec[k];
-        T v;
-        if (WAIT) {
-            v = ld_relaxed_val(x + c);
-            while (Sentinel<T>::is(v)) v = ld_relaxed_val(x + c);
-        } else {
-            v = ld_cg(x + c);
+    int cn[U];
+    T an[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int k = u * 32 + lane;
+        cn[u] = k < width ? ld_stream(ec + k) : -1;
+        an[u] = k < width ? ld_stream(ev + k) : T(0);
+    }
+    for (int base = 0; base < width; base += 32 * U) {
+        int c[U];
+        T a[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            c[u] = cn[u];
+            a[u] = an[u];
         }
-        acc = __fma_rn(ld_stream(ev + k), v, acc);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            v[u] = c[u] >= 0 ? (WAIT ? ld_relaxed_val(x + c[u]) : ld_cg(x + c[u])) : T(0);
+        if (base + 32 * U < width) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k = base + 32 * U + u * 32 + lane;
+                cn[u] = k < width ? ld_stream(ec + k) : -1;
+                an[u] = k < width ? ld_stream(ev + k) : T(0);
+            }
+        }
+        if (WAIT) {
+            while (pending_any<T, U>(c, v)) {
+                __nanosleep(20);
+                reload_pending<T, U>(c, v, x);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] >= 0) acc = __fma_rn(a[u], v[u], acc);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-        const T r = finish<T, UNIT>(ld_cg(b + row) - acc, invd[cd.pos]);
-        if (WAIT) st_relaxed_val(x + row, Sentinel<T>::scrub(r));
+        const T r = finish<T, UNIT>(bi - acc, di);
+        if (WAIT) {
+            st_relaxed_val(x + row, Sentinel<T>::scrub(r));
+            trace_pub(row);
+        }
         else x[row] = r;
     }
 }
 
 // ---------------------------------------------------------------- SELF
 // x must hold Sentinel<T> in every row on entry (k_prefill).
-template <typename T, bool UNIT>
+template <typename T, bool UNIT, int U>
 __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__ chunks, int nchunks,
                                                    const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                    const int32_t *__restrict__ ecol, const T *__restrict__ eval,
@@ -168,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
         if (!chunk_wpr(cd.meta))
             tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x);
         else
-            wpr_row<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x);
+            wpr_row<T, UNIT, true, U>(cd, lane, perm, invd, ecol, eval, b, x);
     }
     // the last warp out resets the ticket for the next solve on this stream
     if (lane == 0) {
@@ -688,7 +759,15 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         h->epoch = 1;
     }
     if (nrhs == 1) {
-        if (h->self_grid == 0) h->self_grid = resident_grid(k_self<T, UNIT>, h->num_sms);
+        // WPR batch depth: 8 dependency loads in flight per lane (2 CTAs/SM) or,
+        // with SPTRSV_WPR_U=16, 16 (1 CTA/SM)
+        const char *eu = getenv("SPTRSV_WPR_U");
+        const bool u16 = eu && atoi(eu) == 16;
+        auto kself = u16 ? k_self<T, UNIT, 16> : k_self<T, UNIT, 8>;
+        if (h->self_grid == 0 || h->self_u16 != u16) {
+            h->self_grid = resident_grid(kself, h->num_sms);
+            h->self_u16 = u16;
+        }
         const int grid = h->self_grid;
         if ((const void *)b == (const void *)x) {   // in place: keep b aside, x becomes the flag array
             sptrsv_status_t st = ensure_scratch(h, (size_t)h->n * sizeof(T));
@@ -697,7 +776,7 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             b = (const T *)h->d_scratch;
         }
         k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n);
-        k_self<T, UNIT><<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
+        kself<<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
                                                   h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
                                                   (unsigned)(grid * (kThreads / 32)));
     } else {
@@ -719,7 +798,8 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             if (nrhs <= 128) return launch_tile_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
             return SPTRSV_ERR_NOT_SUPPORTED;
         }
-        const bool lv = h->algo != SPTRSV_ALGO_SELF;     // BLOCK / TILE: level-scheduled multi-RHS
+        // SELF / SLFC: self-scheduled multi-RHS; LEVEL / LEVC / BLOCK / TILE: level-scheduled
+        const bool lv = h->algo != SPTRSV_ALGO_SELF && h->algo != SPTRSV_ALGO_SLFC;
         if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
         if (nrhs <= 64) return lv ? launch_level_mrhs<T, UNIT, 2>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
         if (nrhs <= 128) return lv ? launch_level_mrhs<T, UNIT, 4>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
@@ -732,7 +812,12 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
 
 }  // namespace
 
+sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s) {
+    return h->dtype == SPTRSV_F64 ? build_mr<double>(h, s) : build_mr<float>(h, s);
+}
+
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s) {
+    if (nrhs == 1 && (h->algo == SPTRSV_ALGO_SLFC || h->algo == SPTRSV_ALGO_LEVC)) return column_solve(h, b, x, s);
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_BLOCK) return block_solve(h, b, x, s);
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_TILE) return tile_solve(h, b, x, s);
     if (h->dtype == SPTRSV_F64) {
@@ -744,3 +829,8 @@ sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nr
 }
 
 }  // namespace sptrsv
+
+extern "C" int sptrsv_dbg_self_trace(void *dev_buf) {
+    unsigned long long *p = (unsigned long long *)dev_buf;
+    return cudaMemcpyToSymbol(sptrsv::g_tpub, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
+}

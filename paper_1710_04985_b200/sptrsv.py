@@ -21,8 +21,9 @@ LIB_PATH = _build.LIB
 LOWER, UPPER = 0, 1
 NON_UNIT, UNIT = 0, 1
 F64, F32 = 0, 1
-ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_TILE = 0, 1, 2, 3, 4
-ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK, "auto": ALGO_AUTO, "tile": ALGO_TILE}
+ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_TILE, ALGO_SLFC, ALGO_LEVC = 0, 1, 2, 3, 4, 5, 6
+ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK, "auto": ALGO_AUTO, "tile": ALGO_TILE,
+         "slfc": ALGO_SLFC, "levc": ALGO_LEVC}
 UPLO = {"lower": LOWER, "upper": UPPER}
 DIAG = {"non_unit": NON_UNIT, "unit": UNIT}
 

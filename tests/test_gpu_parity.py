@@ -419,3 +419,84 @@ def test_lean_block_random_and_integer(S, seed, uplo, diag, monkeypatch):
     sv.solve(bt, x=bt)
     torch.cuda.synchronize()
     assert np.array_equal(bt.cpu().numpy(), xt)
+
+
+# ------------------------------------------------------------ column-wise SLFC / LEVC (NEXT-1)
+COL_ALGOS = ["slfc", "levc"]
+
+
+@pytest.mark.parametrize("algo", COL_ALGOS)
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_column_full_configs(S, cfg, algo):
+    """Alg. SLFC / LEVC at the full BASELINE sizes:
+    atomics accumulate in arrival order, so parity is by the north-star tolerance."""
+    m, p = workloads.config(cfg)
+    b = workloads.rhs(m.n, 1, seed=p["seed"])[:, 0]
+    ref = oracle.solve(m, b, p["uplo"], p["diag"])
+    x, sv = gpu_solve(S, m, b, p["uplo"], p["diag"], algo=algo)
+    assert sv.info()["algo"] == {"slfc": 5, "levc": 6}[algo]
+    assert relerr(x, ref) <= 1e-10
+
+
+@pytest.mark.parametrize("algo", COL_ALGOS)
+def test_column_cfg3_pair(S, algo):
+    m, p = workloads.config(3)
+    b = workloads.rhs(m.n, 1, seed=p["seed"])[:, 0]
+    y = oracle.solve(m, b, "lower", "unit")
+    ref = oracle.solve(m, y, "upper", "non_unit")
+    lo = S.from_csr(m, "lower", "unit", algo=algo)
+    up = S.from_csr(m, "upper", "non_unit", algo=algo)
+    bt = torch.from_numpy(b).cuda()
+    x = up.solve(lo.solve(bt))
+    torch.cuda.synchronize()
+    assert relerr(x.cpu().numpy(), ref) <= 1e-10
+
+
+@pytest.mark.parametrize("algo", COL_ALGOS)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("uplo,diag", [("lower", "non_unit"), ("upper", "non_unit"), ("lower", "unit"),
+                                       ("upper", "unit")])
+def test_column_random_small(S, uplo, diag, dtype, algo):
+    for seed in range(3):
+        m = random_triangular_fast(3000 + 517 * seed, 3.0 + 2 * seed, seed, uplo)
+        b = workloads.rhs(m.n, 1, seed=seed)[:, 0]
+        ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, diag, dtype=dtype)
+        x, _ = gpu_solve(S, m, b, uplo, diag, dtype=dtype, algo=algo)
+        assert relerr(x, ref) <= TOL[dtype]
+        if dtype == np.float64:                        # and the column-wise sweep (P:189-206)
+            assert relerr(x, oracle.solve_col(m, b, uplo, diag)) <= 1e-10
+
+
+@pytest.mark.parametrize("algo", COL_ALGOS)
+@pytest.mark.parametrize("uplo", ["lower", "upper"])
+def test_column_integer_exact_in_place_and_repeat(S, uplo, algo):
+    """Integer systems with power-of-two diagonals are exact in any summation
+    order: atomics included, the result is bitwise x_true, every solve."""
+    m = workloads.stencil((40, 30, 20), 7, uplo, diag=8.0)
+    xt = workloads.integer_xtrue(m.n, 1, seed=101)[:, 0]
+    b = oracle.matvec(m, xt, uplo)
+    x, sv = gpu_solve(S, m, b, uplo, algo=algo)
+    assert np.array_equal(x, xt)
+    for _ in range(3):                                 # counters / barrier state carried across solves
+        x2, _ = gpu_solve(S, m, b, uplo, solver=sv)
+        assert np.array_equal(x2, xt)
+    bt = torch.from_numpy(b).cuda()
+    sv.solve(bt, x=bt)
+    torch.cuda.synchronize()
+    assert np.array_equal(bt.cpu().numpy(), xt)
+
+
+@pytest.mark.parametrize("algo", COL_ALGOS)
+def test_column_multi_rhs_and_degenerate(S, algo):
+    """nrhs > 1 runs the row kernels; diagonal-only and 1x1 systems."""
+    m = random_triangular_fast(2000, 4.0, 7, "lower")
+    B = workloads.rhs(m.n, 5, seed=7)
+    ref = oracle.solve(m, B, "lower")
+    sv = S.from_csr(m, algo=algo)
+    X = sv.solve(torch.from_numpy(B).cuda()).cpu().numpy()
+    assert relerr(X, ref) <= 1e-10
+    for n in (1, 37):
+        d = CSR(n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), np.full(n, 4.0))
+        bb = np.arange(1, n + 1, dtype=np.float64)
+        x, _ = gpu_solve(S, d, bb, algo=algo)
+        assert np.array_equal(x, bb / 4.0)

@@ -228,3 +228,46 @@ def test_ignored_entries_counted():
     # solving with the full A and uplo=lower equals solving with L+D
     b = workloads.rhs(a.n, 1, 5)
     assert np.array_equal(oracle.solve(a, b, "lower"), oracle.solve(lo, b, "lower"))
+
+
+# ------------------------------------------------ column-wise sweep, reference of SLFC / LEVC
+@pytest.mark.parametrize("seed", range(20))
+def test_solve_col_matches_dense_trtrs(seed):
+    """Pinned to LAPACK trtrs on the dense triangle (not to the row oracle)."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(1, 200))
+    uplo = ("lower", "upper")[seed % 2]
+    diag = ("non_unit", "unit")[(seed // 2) % 2]
+    m = random_triangular(n, float(rng.uniform(0.01, 0.2)), seed, uplo, extra_other=0.05)
+    if diag == "unit":
+        m.vals[m.colidx != np.repeat(np.arange(n), np.diff(m.rowptr))] *= 0.3 / max(1, n ** 0.5)
+    b = rng.uniform(-1, 1, size=n)
+    x = oracle.solve_col(m, b, uplo, diag)
+    ref = scipy.linalg.solve_triangular(dense_triangle(m, uplo, diag), b, lower=(uplo == "lower"))
+    assert np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-300) <= 1e-12
+
+
+@pytest.mark.parametrize("uplo", ["lower", "upper"])
+def test_solve_col_integer_exact(uplo):
+    m = workloads.stencil((12, 10, 9), 7, uplo, diag=8.0)
+    xt = workloads.integer_xtrue(m.n, 1, seed=103)[:, 0]
+    b = oracle.matvec(m, xt, uplo)
+    assert np.array_equal(oracle.solve_col(m, b, uplo), xt)
+
+
+def test_solve_col_hand_example():
+    """3x3 lower, by hand: L = [[2,0,0],[1,4,0],[3,-2,8]], f = [2,9,17]
+    column 1: x1 = 2/2 = 1; x2 = 9-1 = 8, x3 = 17-3 = 14
+    column 2: x2 = 8/4 = 2; x3 = 14+4 = 18;  column 3: x3 = 18/8 = 2.25"""
+    m = CSR(3, np.array([0, 1, 3, 6], dtype=np.int32), np.array([0, 0, 1, 0, 1, 2], dtype=np.int32),
+            np.array([2.0, 1.0, 4.0, 3.0, -2.0, 8.0]))
+    assert np.array_equal(oracle.solve_col(m, np.array([2.0, 9.0, 17.0])), np.array([1.0, 2.0, 2.25]))
+    # unit diagonal ignores the stored 2, 4, 8; the upper part is not referenced
+    assert np.array_equal(oracle.solve_col(m, np.array([2.0, 9.0, 17.0]), "lower", "unit"),
+                          np.array([2.0, 7.0, 25.0]))
+
+
+def test_solve_col_zero_pivot_status():
+    m = CSR(2, np.array([0, 1, 2], dtype=np.int32), np.array([0, 0], dtype=np.int32), np.array([1.0, 1.0]))
+    with pytest.raises(oracle.OracleError):
+        oracle.solve_col(m, np.ones(2))
