@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--extra", action="store_true", help="also time the other algos and print them")
+    ap.add_argument("--no-cusparse", action="store_true", help="skip the cuSPARSE SpSV context timing")
     return ap.parse_args()
 
 
@@ -352,6 +353,43 @@ def run_ours(args):
                "d2h_bytes_per_step": int(hb.numel() * esize * len(handles)),
                "ms_per_step": round(t_e2e * 1e3, 4), "api": "sptrsv_solve_host"}
 
+    # cuSPARSE SpSV on the same problem, same protocol (context)
+    cusp = None
+    if not args.no_cusparse and world == 1 and nrhs == 1:
+        try:
+            import baseline
+            npdt = np.float64 if args.dtype == "f64" else np.float32
+            cbufs = [torch.empty_like(b) for _ in handles]
+            ctxs, z = [], b
+            for (uplo, diag), out in zip(solves, cbufs):
+                ctxs.append(baseline.CusparseSpSV(m, uplo, diag, z, out, npdt))
+                z = out
+            sp = stream.cuda_stream
+            for _ in range(3):
+                for c in ctxs:
+                    c.solve(sp)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(max(5, args.steps // 2)):
+                if flush is not None:
+                    flush.zero_()
+                a_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+                for c in ctxs:
+                    c.solve(sp)
+                e_.record(stream)
+                e_.synchronize()
+                ts.append(a_.elapsed_time(e_) / 1e3)
+            tc = float(np.mean(ts))
+            ours = bufs[-1].double()
+            diff = float((cbufs[-1].double() - ours).abs().max() / ours.abs().max().clamp_min(1e-300))
+            cusp = {"us_per_step": round(tc * 1e6, 2), "GB/s": round(nbytes / tc / 1e9, 2),
+                    "speedup_ours": round(tc / t_mean, 3), "max_rel_diff_vs_ours": diff,
+                    "api": "cusparseSpSV_solve (CUSPARSE_SPSV_ALG_DEFAULT), analysis outside the timing"}
+            del ctxs
+        except Exception as e:              # context only: never fails the bench
+            cusp = {"unavailable": str(e)[:200]}
+
     # extra: the other algorithms on the same problem (context, rank 0 prints)
     extra = {}
     if args.extra and world == 1:
@@ -434,6 +472,8 @@ def run_ours(args):
     }
     if extra:
         line["extra_algos"] = extra
+    if cusp is not None:
+        line["cusparse_spsv"] = cusp
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
