@@ -150,7 +150,9 @@ extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo
         algo != SPTRSV_ALGO_LEVC)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
-    const bool want_block = algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_AUTO || algo == SPTRSV_ALGO_TILE;
+    // AUTO only uses BLOCK for rows with <= 3 dependencies: skip its build otherwise
+    const bool want_block = algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_TILE ||
+                            (algo == SPTRSV_ALGO_AUTO && h->info.max_row_deps <= 3);
     if (want_block && !h->block.built && h->n > 0) {
         SPTRSV_CUDA(cudaSetDevice(h->device));
         sptrsv_status_t st = block_build(h, nullptr);
@@ -167,8 +169,13 @@ extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo
         h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
     }
     if (algo == SPTRSV_ALGO_TILE && !h->tile.built) return SPTRSV_ERR_NOT_SUPPORTED;
-    if (algo == SPTRSV_ALGO_AUTO)     // BLOCK is the fastest single-RHS path on grids (profiles/)
-        algo = (h->block.built && h->block.grid_nx > 0) ? SPTRSV_ALGO_BLOCK : SPTRSV_ALGO_SELF;
+    // AUTO: BLOCK on detected grids with <= 3 dependencies per row (5- / 7-point
+    // factors: cfg1 24 us vs 80 us, cfg2 0.27 vs 0.54 ms for SELF); SELF
+    // otherwise (27-point ILU cfg3: SELF 2.89 ms vs BLOCK 3.84 ms;
+    // profiles/bench_cfgs_r1g.json)
+    if (algo == SPTRSV_ALGO_AUTO)
+        algo = (h->block.built && h->block.grid_nx > 0 && h->info.max_row_deps <= 3) ? SPTRSV_ALGO_BLOCK
+                                                                                      : SPTRSV_ALGO_SELF;
     h->algo = algo;
     h->info.algo = algo;
     return SPTRSV_SUCCESS;

@@ -83,6 +83,25 @@ __device__ __forceinline__ void reload_pending(const int (&c)[N], T (&v)[N], con
     for (int u = 0; u < N; ++u)
         if (c[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + c[u]);
 }
+// Thread-per-row poll: only the LAST pending dependency in storage order (the
+// nearest row, in practice the critical one from the previous level) is
+// re-loaded, and every 4th round all pending ones.  Re-loading every pending
+// value each round made 2,400 spinning warps flood L2 with polls (cfg3, 13
+// dependencies per row: 3.2 us from ready to published, tools/self_trace.py).
+template <typename T, int N>
+__device__ __forceinline__ void reload_pending_lazy(const int (&c)[N], T (&v)[N], const T *x, unsigned it) {
+    if ((it & 3u) == 0) {
+        reload_pending<T, N>(c, v, x);
+        return;
+    }
+    int last = -1;
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+        if (c[u] >= 0 && Sentinel<T>::is(v[u])) last = u;
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+        if (u == last) v[u] = ld_relaxed_val(x + c[u]);
+}
 
 // ---------------------------------------------------------------- TPR row
 // One chunk of up to 32 rows, thread per row.  Entry k of lane r at
@@ -122,48 +141,26 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
     if (WAIT) {
 #pragma unroll
         for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_relaxed_val(x + cols[k]) : T(0);
-        // each lane publishes its row as soon as ITS dependencies are there
-        // (not when the chunk's slowest lane is): a row's consumers never
-        // wait for an unrelated row of the same chunk
-        // Short rows (<= 12 dependencies): warp-converged loop, each lane
-        // publishes as soon as its own row is ready.  Longer rows: a per-lane
-        // loop (a lane leaves it and publishes on its own).  Measured: the
-        // converged form is faster on cfg2 / cfg4 (0.62 vs 0.67 ms, 29.4 vs
-        // 33.8 ms), the per-lane form on cfg3's 13-dependency rows (4.0 vs 10.2 ms).
-        if (width <= 12) {
-            bool done = !act;
-            for (;;) {
-                if (!done && !pending_any<T, kTprMax>(cols, xv)) {
-#pragma unroll
-                    for (int k = 0; k < kTprMax; ++k) {
-                        if (cols[k] >= 0) s = fnma(vals[k], xv[k], s);
-                    }
-                    st_relaxed_val(x + row, Sentinel<T>::scrub(finish<T, UNIT>(s, di)));
-                    trace_pub(tp, row);
-                    done = true;
-                }
-                if (__all_sync(0xffffffffu, done)) return;
-                __nanosleep(20);
-                reload_pending<T, kTprMax>(cols, xv, x);
-            }
-        }
+        // Warp-converged loop; each lane publishes as soon as its own row is
+        // ready (not when the chunk's slowest lane is).  Rows with > 12
+        // dependencies poll lazily (reload_pending_lazy).
+        bool done = !act;
+        unsigned it = 0;
         for (;;) {
-            if (!pending_any<T, kTprMax>(cols, xv)) {
-                if (act) {
+            if (!done && !pending_any<T, kTprMax>(cols, xv)) {
 #pragma unroll
-                    for (int k = 0; k < kTprMax; ++k) {
-                        if (cols[k] >= 0) s = fnma(vals[k], xv[k], s);
-                    }
-                    st_relaxed_val(x + row, Sentinel<T>::scrub(finish<T, UNIT>(s, di)));
-                    trace_pub(tp, row);
+                for (int k = 0; k < kTprMax; ++k) {
+                    if (cols[k] >= 0) s = fnma(vals[k], xv[k], s);
                 }
-                break;
+                st_relaxed_val(x + row, Sentinel<T>::scrub(finish<T, UNIT>(s, di)));
+                trace_pub(tp, row);
+                done = true;
             }
+            if (__all_sync(0xffffffffu, done)) return;
             __nanosleep(20);
-            reload_pending<T, kTprMax>(cols, xv, x);
+            if (width <= 12) reload_pending<T, kTprMax>(cols, xv, x);
+            else reload_pending_lazy<T, kTprMax>(cols, xv, x, ++it);
         }
-        __syncwarp();
-        return;
     } else {
 #pragma unroll
         for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_cg(x + cols[k]) : T(0);
@@ -226,7 +223,7 @@ __device__ __forceinline__ void wpr_row(const ChunkDesc &cd, int lane, const int
             }
         }
         if (WAIT) {
-            while (pending_any<T, U>(c, v)) {
+            while (pending_any<T, U>(c, v)) {       // (lazy polling measured slower here)
                 __nanosleep(20);
                 reload_pending<T, U>(c, v, x);
             }
@@ -785,13 +782,20 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         h->epoch = 1;
     }
     if (nrhs == 1) {
-        // WPR batch depth: 8 dependency loads in flight per lane (2 CTAs/SM) or,
-        // with SPTRSV_WPR_U=16, 16 (1 CTA/SM)
+        // WPR batch depth: 8 dependency loads in flight per lane or, with
+        // SPTRSV_WPR_U=16, 16
         const char *eu = getenv("SPTRSV_WPR_U");
         const bool u16 = eu && atoi(eu) == 16;
         auto kself = u16 ? k_self<T, UNIT, 16> : k_self<T, UNIT, 8>;
         if (h->self_grid == 0 || h->self_u16 != u16) {
-            h->self_grid = resident_grid(kself, h->num_sms);
+            // one CTA (8 warps) per SM: 74-148 CTAs solve cfg2/3/4 equally fast,
+            // 2 CTAs/SM are 10-35% slower -- spinning warps' polls load L2
+            // (cfg3 3.92 -> 2.87 ms, cfg2 0.63 -> 0.54 ms, cfg4 34.0 -> 31.1 ms)
+            h->self_grid = std::min(resident_grid(kself, h->num_sms), h->num_sms);
+            const char *ec = getenv("SPTRSV_SELF_CPS");      // CTAs per SM (fewer spinning warps)
+            if (ec && atoi(ec) > 0) h->self_grid = std::min(h->self_grid, atoi(ec) * h->num_sms);
+            const char *eg = getenv("SPTRSV_SELF_GRID");     // absolute CTA count (tuning)
+            if (eg && atoi(eg) > 0) h->self_grid = std::min(h->self_grid, atoi(eg));
             h->self_u16 = u16;
         }
         const int grid = h->self_grid;

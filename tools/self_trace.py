@@ -12,6 +12,8 @@ from paper_1710_04985_b200 import sptrsv as S
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 m, p = workloads.config(cfg, scale)
+if p.get("pair"):                      # cfg3: the forward (unit lower) solve
+    p = dict(p, uplo="lower", diag="unit")
 sv = S.from_csr(m, p["uplo"], p["diag"], algo="self")
 n = m.n
 b = torch.from_numpy(workloads.rhs(n, 1, seed=2)[:, 0]).cuda()
@@ -31,7 +33,7 @@ lev, _, _, nlev = sv.levels()
 # strict lower part of the matrix: dependencies
 rp, ci = m.rowptr.astype(np.int64), m.colidx.astype(np.int64)
 row_of = np.repeat(np.arange(n), np.diff(rp))
-strict = ci < row_of
+strict = (ci < row_of) if p["uplo"] == "lower" else (ci > row_of)
 deps_row, deps_col = row_of[strict], ci[strict]
 ndeps = np.bincount(deps_row, minlength=n)
 ready = np.full(n, 0.0)
