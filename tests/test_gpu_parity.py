@@ -500,3 +500,19 @@ def test_column_multi_rhs_and_degenerate(S, algo):
         bb = np.arange(1, n + 1, dtype=np.float64)
         x, _ = gpu_solve(S, d, bb, algo=algo)
         assert np.array_equal(x, bb / 4.0)
+
+
+def test_auto_selection_rule(S):
+    """AUTO: BLOCK on detected grids with <= 3 dependencies per row (5-/7-point
+    factors), SELF otherwise (27-point ILU, general matrices)."""
+    m7 = workloads.stencil((24, 20, 16), 7, "lower")
+    assert S.from_csr(m7, algo="auto").info()["algo"] == 2
+    m5 = workloads.stencil((40, 30), 5, "upper")
+    assert S.from_csr(m5, "upper", algo="auto").info()["algo"] == 2
+    m27 = workloads.ilu0(workloads.stencil((12, 10, 8), 27, "full"))
+    for uplo, diag in (("lower", "unit"), ("upper", "non_unit")):
+        sv = S.from_csr(m27, uplo, diag, algo="auto")
+        assert sv.info()["algo"] == 0
+        b = workloads.rhs(m27.n, 1, seed=9)[:, 0]
+        x, _ = gpu_solve(S, m27, b, uplo, diag, solver=sv)
+        assert relerr(x, oracle.solve(m27, b, uplo, diag)) <= 1e-10
