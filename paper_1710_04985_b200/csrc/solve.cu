@@ -114,7 +114,7 @@ template <typename T, bool UNIT, bool WAIT>
 __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                           const T *__restrict__ invd, const int32_t *__restrict__ ecol,
                                           const T *__restrict__ eval, const T *b, T *x,
-                                          unsigned long long *tp = nullptr) {
+                                          unsigned long long *tp = nullptr, int lazy_w = kTprMax) {
     const int nr = chunk_nrows(cd.meta), width = chunk_width(cd.meta);
     const bool act = lane < nr;
     int row = 0;
@@ -142,8 +142,8 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
 #pragma unroll
         for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_relaxed_val(x + cols[k]) : T(0);
         // Warp-converged loop; each lane publishes as soon as its own row is
-        // ready (not when the chunk's slowest lane is).  Rows with > 12
-        // dependencies poll lazily (reload_pending_lazy).
+        // ready (not when the chunk's slowest lane is).  Rows with more than
+        // lazy_w dependencies poll lazily (reload_pending_lazy; off by default).
         bool done = !act;
         unsigned it = 0;
         for (;;) {
@@ -158,7 +158,7 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
             }
             if (__all_sync(0xffffffffu, done)) return;
             __nanosleep(20);
-            if (width <= 12) reload_pending<T, kTprMax>(cols, xv, x);
+            if (width <= lazy_w) reload_pending<T, kTprMax>(cols, xv, x);
             else reload_pending_lazy<T, kTprMax>(cols, xv, x, ++it);
         }
     } else {
@@ -250,7 +250,8 @@ template <typename T, bool UNIT, int U>
 __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__ chunks, int nchunks,
                                                    const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                    const int32_t *__restrict__ ecol, const T *__restrict__ eval,
-                                                   const T *b, T *x, unsigned *ctr, unsigned nwarps_total) {
+                                                   const T *b, T *x, unsigned *ctr, unsigned nwarps_total,
+                                                   int lazy_w) {
     const int lane = threadIdx.x & 31;
     unsigned long long *tp = g_tpub;         // debug trace (read once)
     for (;;) {
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
         if ((int)t >= nchunks) break;
         const ChunkDesc cd = chunks[t];
         if (!chunk_wpr(cd.meta))
-            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp);
+            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp, lazy_w);
         else
             wpr_row<T, UNIT, true, U>(cd, lane, perm, invd, ecol, eval, b, x, tp);
     }
@@ -799,6 +800,11 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             h->self_u16 = u16;
         }
         const int grid = h->self_grid;
+        // TPR rows wider than lazy_w poll lazily (SPTRSV_TPR_LAZY_W); default
+        // never: with one CTA per SM, polling every pending dependency is faster
+        // (cfg4 26.8 vs 31.2 ms, cfg3 2.46 vs 2.91 ms with lazy_w = 12)
+        const char *elw = getenv("SPTRSV_TPR_LAZY_W");
+        const int lazy_w = elw ? atoi(elw) : kTprMax;
         if ((const void *)b == (const void *)x) {   // in place: keep b aside, x becomes the flag array
             sptrsv_status_t st = ensure_scratch(h, (size_t)h->n * sizeof(T));
             if (st != SPTRSV_SUCCESS) return st;
@@ -808,7 +814,7 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n);
         kself<<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
                                                   h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
-                                                  (unsigned)(grid * (kThreads / 32)));
+                                                  (unsigned)(grid * (kThreads / 32)), lazy_w);
     } else {
         if (!h->mr_built) {
             sptrsv_status_t st = build_mr<T>(h, s);
