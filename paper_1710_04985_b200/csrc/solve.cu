@@ -114,7 +114,8 @@ template <typename T, bool UNIT, bool WAIT>
 __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                           const T *__restrict__ invd, const int32_t *__restrict__ ecol,
                                           const T *__restrict__ eval, const T *b, T *x,
-                                          unsigned long long *tp = nullptr, int lazy_w = kTprMax) {
+                                          unsigned long long *tp = nullptr, int lazy_w = kTprMax,
+                                          unsigned sleep_ns = 20) {
     const int nr = chunk_nrows(cd.meta), width = chunk_width(cd.meta);
     const bool act = lane < nr;
     int row = 0;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
                 done = true;
             }
             if (__all_sync(0xffffffffu, done)) return;
-            __nanosleep(20);
+            if (sleep_ns > 0) __nanosleep(sleep_ns);
             if (width <= lazy_w) reload_pending<T, kTprMax>(cols, xv, x);
             else reload_pending_lazy<T, kTprMax>(cols, xv, x, ++it);
         }
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
                                                    const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                    const int32_t *__restrict__ ecol, const T *__restrict__ eval,
                                                    const T *b, T *x, unsigned *ctr, unsigned nwarps_total,
-                                                   int lazy_w) {
+                                                   int lazy_w, unsigned sleep_ns) {
     const int lane = threadIdx.x & 31;
     unsigned long long *tp = g_tpub;         // debug trace (read once)
     for (;;) {
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
         if ((int)t >= nchunks) break;
         const ChunkDesc cd = chunks[t];
         if (!chunk_wpr(cd.meta))
-            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp, lazy_w);
+            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp, lazy_w, sleep_ns);
         else
             wpr_row<T, UNIT, true, U>(cd, lane, perm, invd, ecol, eval, b, x, tp);
     }
@@ -793,6 +794,12 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             // 2 CTAs/SM are 10-35% slower -- spinning warps' polls load L2
             // (cfg3 3.92 -> 2.87 ms, cfg2 0.63 -> 0.54 ms, cfg4 34.0 -> 31.1 ms)
             h->self_grid = std::min(resident_grid(kself, h->num_sms), h->num_sms);
+            // rows with many dependencies (mean >= 8) poll more values per lane:
+            // half the SMs' worth of warps is enough and loads L2 less
+            // (cfg3, 13 deps/row: 2.47 -> 2.14 ms; cfg4 26.8 -> 26.6 ms; cfg2,
+            // 3 deps/row, prefers 148 CTAs: 0.54 vs 0.62 ms)
+            const int64_t strict = h->info.nnz_used - (h->diag == SPTRSV_NON_UNIT ? (int64_t)h->n : 0);
+            if (h->n > 0 && strict >= 8 * (int64_t)h->n) h->self_grid = std::max(1, h->self_grid / 2);
             const char *ec = getenv("SPTRSV_SELF_CPS");      // CTAs per SM (fewer spinning warps)
             if (ec && atoi(ec) > 0) h->self_grid = std::min(h->self_grid, atoi(ec) * h->num_sms);
             const char *eg = getenv("SPTRSV_SELF_GRID");     // absolute CTA count (tuning)
@@ -805,6 +812,8 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         // (cfg4 26.8 vs 31.2 ms, cfg3 2.46 vs 2.91 ms with lazy_w = 12)
         const char *elw = getenv("SPTRSV_TPR_LAZY_W");
         const int lazy_w = elw ? atoi(elw) : kTprMax;
+        const char *esl = getenv("SPTRSV_SELF_SLEEP");      // ns between TPR polls
+        const unsigned sleep_ns = esl ? (unsigned)atoi(esl) : 20u;
         if ((const void *)b == (const void *)x) {   // in place: keep b aside, x becomes the flag array
             sptrsv_status_t st = ensure_scratch(h, (size_t)h->n * sizeof(T));
             if (st != SPTRSV_SUCCESS) return st;
@@ -814,7 +823,7 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n);
         kself<<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
                                                   h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
-                                                  (unsigned)(grid * (kThreads / 32)), lazy_w);
+                                                  (unsigned)(grid * (kThreads / 32)), lazy_w, sleep_ns);
     } else {
         if (!h->mr_built) {
             sptrsv_status_t st = build_mr<T>(h, s);
