@@ -22,6 +22,7 @@
 // parity is by the north-star tolerance.  Same division reading as the row
 // kernels (Q7): multiply by 1/d.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kColThreads) k_slfc(int n, const int32_t *__re
                                                       const int32_t *__restrict__ cptr,
                                                       const int32_t *__restrict__ crow,
                                                       const T *__restrict__ cval, T *x, int32_t *count,
-                                                      unsigned *ctr, unsigned nwarps_total) {
+                                                      unsigned *ctr, unsigned nwarps_total, int rel_each) {
     const int lane = threadIdx.x & 31;
     const int nblk = (n + 31) / 32;
     for (;;) {
@@ -120,9 +121,14 @@ __global__ void __launch_bounds__(kColThreads) k_slfc(int n, const int32_t *__re
             const int k0 = cptr[i], k1 = cptr[i + 1];
             column_update<T, UNIT>(i, invd_row, cptr, crow, cval, x);
             if (k1 > k0) {
-                // the x updates above happen before any counter decrement below
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                for (int k = k0; k < k1; ++k) red_dec(count + crow[k]);
+                if (rel_each) {        // release on every decrement instead of one fence
+                    for (int k = k0; k < k1; ++k)
+                        asm volatile("red.release.gpu.global.add.s32 [%0], -1;" ::"l"(count + crow[k]) : "memory");
+                } else {
+                    // the x updates above happen before any counter decrement below
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    for (int k = k0; k < k1; ++k) red_dec(count + crow[k]);
+                }
             }
         }
     }
@@ -221,12 +227,15 @@ sptrsv_status_t launch_column(sptrsv_handle_t h, const T *b, T *x, cudaStream_t 
             SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_slfc<T, UNIT>, kColThreads, 0));
             // at most 2 CTAs (16 warps) per SM: enough columns in flight, and
             // not so many spinning lanes that their polls slow the L2
-            h->slfc_grid = std::max(1, std::min(per_sm, 2)) * h->num_sms;
+            const char *ec = getenv("SPTRSV_SLFC_CPS");
+            const int cps = (ec && atoi(ec) > 0) ? atoi(ec) : 1;   // 1/SM: 2-6% faster than 2
+            h->slfc_grid = std::max(1, std::min(per_sm, cps)) * h->num_sms;
         }
         const int grid = h->slfc_grid;
         k_slfc<T, UNIT><<<grid, kColThreads, 0, s>>>(n, h->d_perm, (const T *)h->d_invd_row, h->d_c_ptr, h->d_c_row,
                                                     (const T *)h->d_c_val, x, h->d_count, h->d_ctr,
-                                                    (unsigned)(grid * (kColThreads / 32)));
+                                                    (unsigned)(grid * (kColThreads / 32)),
+                                                    getenv("SPTRSV_SLFC_REL") ? atoi(getenv("SPTRSV_SLFC_REL")) : 0);
         SPTRSV_CUDA(cudaGetLastError());
         return SPTRSV_SUCCESS;
     }

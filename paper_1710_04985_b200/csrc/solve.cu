@@ -737,6 +737,8 @@ sptrsv_status_t launch_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaS
         int per_sm = 0;
         SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mrhs<T, UNIT, CPL>, kThreads, 0));
         grid = std::max(1, per_sm) * h->num_sms;
+        const char *eg = getenv("SPTRSV_MRHS_GRID");      // tuning: absolute CTA count
+        if (eg && atoi(eg) > 0) grid = std::min(grid, atoi(eg));
     }
     k_mrhs<T, UNIT, CPL><<<grid, kThreads, 0, s>>>(h->n, h->d_perm, h->d_lev, (const T *)h->d_invd, h->d_mr_ptr,
                                                    h->d_mr_col,
