@@ -335,6 +335,99 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level(const ChunkDesc *__r
 // column equals the nrhs == 1 TPR result bitwise and does not depend on nrhs
 // (SURVEY §8e partition invariant).  Entries come from a per-position CSR
 // (mr_*), built on the first multi-RHS solve.
+// Multi-RHS with per-(row, column) value-as-flag (k_mrhs_vf, nrhs <= 16):
+// x is prefilled with the sentinel; a warp claims 32/W rows by ticket in
+// solve order (W = nrhs rounded up to a power of two), lane = (row slot,
+// column).  A lane polls only ITS column of its row's dependencies (relaxed
+// loads, all in flight at once) and publishes x(row, column) with a relaxed
+// store: no flags, no fences -- the SELF protocol per column.  Per column the
+// arithmetic is the TPR sequence (bitwise equal to the other multi-RHS
+// kernels and to nrhs == 1).  The level-scheduled kernel costs ~4.5 us per
+// level whatever nrhs is (tools/mrhs_sweep.py), so for the few columns of a
+// multi-GPU rank (cfg5: 64/G) this is the faster path.
+template <typename T, bool UNIT, int W>
+__global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__restrict__ perm,
+                                                      const T *__restrict__ invd,
+                                                      const int32_t *__restrict__ mr_ptr,
+                                                      const int32_t *__restrict__ mr_col,
+                                                      const T *__restrict__ mr_val, const T *b, T *x, int nrhs,
+                                                      unsigned *ctr, unsigned nwarps_total) {
+    constexpr int RPW = 32 / W;               // rows per warp
+    constexpr int DB = 8;                     // dependency loads in flight per lane
+    const int lane = threadIdx.x & 31;
+    const int g = lane / W, c = lane % W;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(&ctr[0], (unsigned)RPW);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if ((int)t >= n) break;
+        const int p = (int)t + g;
+        if (p < n && c < nrhs) {
+            const int row = perm[p];
+            const T di = invd[p];
+            const int e0 = mr_ptr[p], e1 = mr_ptr[p + 1];
+            T acc = ld_cg(b + (int64_t)row * nrhs + c);
+            for (int k0 = e0; k0 < e1; k0 += DB) {
+                int cj[DB];
+                T a[DB], v[DB];
+#pragma unroll
+                for (int u = 0; u < DB; ++u) {
+                    cj[u] = k0 + u < e1 ? mr_col[k0 + u] : -1;
+                    a[u] = k0 + u < e1 ? mr_val[k0 + u] : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < DB; ++u) v[u] = cj[u] >= 0 ? ld_relaxed_val(x + (int64_t)cj[u] * nrhs + c) : T(0);
+                for (;;) {
+                    bool pend = false;
+#pragma unroll
+                    for (int u = 0; u < DB; ++u) pend |= cj[u] >= 0 && Sentinel<T>::is(v[u]);
+                    if (!pend) break;
+                    __nanosleep(20);
+#pragma unroll
+                    for (int u = 0; u < DB; ++u)
+                        if (cj[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + (int64_t)cj[u] * nrhs + c);
+                }
+#pragma unroll
+                for (int u = 0; u < DB; ++u)
+                    if (cj[u] >= 0) acc = fnma(a[u], v[u], acc);
+            }
+            st_relaxed_val(x + (int64_t)row * nrhs + c, Sentinel<T>::scrub(finish<T, UNIT>(acc, di)));
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        const unsigned e = atomicAdd(&ctr[1], 1u);
+        if (e == nwarps_total - 1) {
+            ctr[0] = 0;
+            ctr[1] = 0;
+        }
+    }
+}
+
+sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes);
+template <typename T, bool UNIT>
+sptrsv_status_t launch_mrhs_vf(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
+    const size_t elems = (size_t)h->n * nrhs;
+    if ((const void *)b == (const void *)x) {     // in place: keep b aside, x becomes the flag array
+        sptrsv_status_t st = ensure_scratch(h, elems * sizeof(T));
+        if (st != SPTRSV_SUCCESS) return st;
+        SPTRSV_CUDA(cudaMemcpyAsync(h->d_scratch, b, elems * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        b = (const T *)h->d_scratch;
+    }
+    k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)elems);
+    auto kern = nrhs <= 2 ? k_mrhs_vf<T, UNIT, 2> : nrhs <= 4 ? k_mrhs_vf<T, UNIT, 4>
+              : nrhs <= 8 ? k_mrhs_vf<T, UNIT, 8> : nrhs <= 16 ? k_mrhs_vf<T, UNIT, 16> : k_mrhs_vf<T, UNIT, 32>;
+    const char *eg = getenv("SPTRSV_MRHS_VF_GRID");
+    int per_sm = 0;
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
+    int grid = std::max(1, std::min(per_sm, 4)) * h->num_sms;
+    if (eg && atoi(eg) > 0) grid = std::min(atoi(eg), std::max(1, per_sm) * h->num_sms);
+    kern<<<grid, kThreads, 0, s>>>(h->n, h->d_perm, (const T *)h->d_invd, h->d_mr_ptr, h->d_mr_col,
+                                   (const T *)h->d_mr_val, b, x, nrhs, h->d_ctr, (unsigned)(grid * (kThreads / 32)));
+    SPTRSV_CUDA(cudaGetLastError());
+    return SPTRSV_SUCCESS;
+}
+
 constexpr int kMrG = 4;
 
 template <typename T, bool UNIT, int CPL>
@@ -847,6 +940,14 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         }
         // SELF / SLFC: self-scheduled multi-RHS; LEVEL / LEVC / BLOCK / TILE: level-scheduled
         const bool lv = h->algo != SPTRSV_ALGO_SELF && h->algo != SPTRSV_ALGO_SLFC;
+        // value-as-flag multi-RHS for nrhs <= 16 (cfg5 ranks of 4 / 8 GPUs: 16 RHS
+        // 1.02 vs 1.73 ms, 8 RHS 0.59 vs 1.72 ms for the level-scheduled kernel;
+        // 32 RHS: 2.02 vs 1.74 ms, so not there), unless LEVEL / LEVC was asked
+        // for; SPTRSV_MRHS_VF=0 disables it, =1 also takes 17..32
+        const char *evf = getenv("SPTRSV_MRHS_VF");
+        const int vf_max = evf ? (*evf == '0' ? 0 : 32) : 16;
+        const bool level_req = h->algo == SPTRSV_ALGO_LEVEL || h->algo == SPTRSV_ALGO_LEVC;
+        if (nrhs <= vf_max && !level_req) return launch_mrhs_vf<T, UNIT>(h, b, x, nrhs, s);
         if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
         if (nrhs <= 64) return lv ? launch_level_mrhs<T, UNIT, 2>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
         if (nrhs <= 128) return lv ? launch_level_mrhs<T, UNIT, 4>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
