@@ -31,6 +31,7 @@ namespace {
 
 constexpr int kColThreads = 256;
 constexpr int kLevcThreads = 1024;
+constexpr int kLevcThreadsDefault = 128;   // cfg2 2.98 -> 1.70 ms, cfg3 17.8 -> 6.6 ms vs 1024 (grid barrier cost)
 
 // ------------------------------------------------------------ CSC build
 // entries of the per-position CSR (mr_*: row perm[p], dependency mr_col[k])
@@ -244,7 +245,9 @@ sptrsv_status_t launch_column(sptrsv_handle_t h, const T *b, T *x, cudaStream_t 
     void *args[] = {(void *)&nlev, (void *)&h->d_ilev, (void *)&h->d_perm, (void *)&h->d_invd_row,
                     (void *)&h->d_c_ptr, (void *)&h->d_c_row, (void *)&h->d_c_val, (void *)&x,
                     (void *)&h->d_bar, (void *)&h->bar_base};
-    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_levc<T, UNIT>, grid, kLevcThreads, args, 0, s));
+    const char *elt = getenv("SPTRSV_LEVC_THREADS");
+    const int lt = (elt && atoi(elt) >= 32 && atoi(elt) <= kLevcThreads) ? atoi(elt) / 32 * 32 : kLevcThreadsDefault;
+    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_levc<T, UNIT>, grid, lt, args, 0, s));
     h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
     return SPTRSV_SUCCESS;
 }

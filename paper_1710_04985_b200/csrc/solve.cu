@@ -300,9 +300,14 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *bar, unsigned l
 }
 
 constexpr int kLevelThreads = 1024;
+// k_level (single RHS): 128 threads per CTA.  The grid barrier's two
+// __syncthreads grow with the CTA, and a level of cfg2 keeps only ~170 warps
+// busy: 1024 -> 128 threads took cfg2 2.20 -> 1.55 ms, cfg3 12.1 -> 5.9 ms,
+// cfg4 61.5 -> 55.8 ms (SPTRSV_LEVEL_THREADS overrides).
+constexpr int kLevelThreads1 = 128;
 
 template <typename T, bool UNIT>
-__global__ void __launch_bounds__(kLevelThreads, 1) k_level(const ChunkDesc *__restrict__ chunks,
+__global__ void __launch_bounds__(kLevelThreads1, 1) k_level(const ChunkDesc *__restrict__ chunks,
                                                     const int32_t *__restrict__ lev_chunk, int nlev,
                                                     const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                     const int32_t *__restrict__ ecol, const T *__restrict__ eval,
@@ -848,7 +853,9 @@ sptrsv_status_t launch_level_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs,
     void *args[] = {(void *)&h->d_ilev, (void *)&nlev, (void *)&h->d_perm, (void *)&h->d_invd, (void *)&h->d_mr_ptr,
                     (void *)&h->d_mr_col, (void *)&h->d_mr_val, (void *)&b, (void *)&x, (void *)&nrhs,
                     (void *)&h->d_bar, (void *)&h->bar_base};
-    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level_mrhs<T, UNIT, CPL>, grid, kLevelThreads, args, 0, s));
+    const char *emt = getenv("SPTRSV_LEVEL_MRHS_THREADS");
+    const int mt = (emt && atoi(emt) >= 32 && atoi(emt) <= kLevelThreads) ? atoi(emt) / 32 * 32 : kLevelThreads;
+    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level_mrhs<T, UNIT, CPL>, grid, mt, args, 0, s));
     h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
     return SPTRSV_SUCCESS;
 }
@@ -870,7 +877,9 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         void *args[] = {(void *)&h->d_chunks, (void *)&h->d_lev_chunk, (void *)&nlev, (void *)&h->d_perm,
                         (void *)&h->d_invd, (void *)&h->d_ecol, (void *)&h->d_eval, (void *)&b,
                         (void *)&x, (void *)&h->d_bar, (void *)&h->bar_base};
-        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, kLevelThreads, args, 0, s));
+        const char *elt = getenv("SPTRSV_LEVEL_THREADS");
+        const int lt = (elt && atoi(elt) >= 32 && atoi(elt) <= kLevelThreads1) ? atoi(elt) / 32 * 32 : kLevelThreads1;
+        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, lt, args, 0, s));
         h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
         return SPTRSV_SUCCESS;
     }
