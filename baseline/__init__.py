@@ -32,7 +32,7 @@ def _load():
         vp = ctypes.c_void_p
         lib.spsv_create.restype = ctypes.c_int
         lib.spsv_create.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.c_int,
-                                    ctypes.c_int, vp, vp, ctypes.POINTER(vp)]
+                                    ctypes.c_int, vp, vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_float)]
         lib.spsv_solve.restype = ctypes.c_int
         lib.spsv_solve.argtypes = [vp, vp]
         lib.spsv_destroy.restype = None
@@ -63,9 +63,12 @@ class CusparseSpSV:
         self._keep = [torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(),
                       torch.from_numpy(va.astype(dtype)).cuda(), b, x]
         out = ctypes.c_void_p()
+        an = ctypes.c_float(0.0)
         st = _load().spsv_create(m.n, int(ci.size), self._keep[0].data_ptr(), self._keep[1].data_ptr(),
                                  self._keep[2].data_ptr(), int(uplo == "upper"), int(diag == "unit"),
-                                 int(dtype == np.float32), b.data_ptr(), x.data_ptr(), ctypes.byref(out))
+                                 int(dtype == np.float32), b.data_ptr(), x.data_ptr(), ctypes.byref(out),
+                                 ctypes.byref(an))
+        self.analysis_ms = float(an.value)      # cusparseSpSV_analysis alone (CUDA events)
         if st != 0:
             raise RuntimeError(f"cuSPARSE SpSV setup failed ({st})")
         self.ctx = out

@@ -17,7 +17,7 @@ struct SpsvCtx {
 };
 
 extern "C" int spsv_create(int n, int64_t nnz, const int32_t *rowptr, const int32_t *colidx, const void *vals,
-                           int upper, int unit, int f32, void *b, void *x, void **out) {
+                           int upper, int unit, int f32, void *b, void *x, void **out, float *analysis_ms) {
     SpsvCtx *c = new SpsvCtx;
     c->t = f32 ? CUDA_R_32F : CUDA_R_64F;
     if (cusparseCreate(&c->h) != CUSPARSE_STATUS_SUCCESS) return 1;
@@ -39,9 +39,20 @@ extern "C" int spsv_create(int n, int64_t nnz, const int32_t *rowptr, const int3
                                 CUSPARSE_SPSV_ALG_DEFAULT, c->d, &bytes) != CUSPARSE_STATUS_SUCCESS)
         return 4;
     if (cudaMalloc(&c->buf, bytes > 0 ? bytes : 16) != cudaSuccess) return 5;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, 0);
     if (cusparseSpSV_analysis(c->h, CUSPARSE_OPERATION_NON_TRANSPOSE, alpha, c->A, c->X, c->Y, c->t,
                               CUSPARSE_SPSV_ALG_DEFAULT, c->d, c->buf) != CUSPARSE_STATUS_SUCCESS)
         return 6;
+    cudaEventRecord(e1, 0);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (analysis_ms) *analysis_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     *out = c;
     return 0;
 }

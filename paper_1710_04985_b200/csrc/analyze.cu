@@ -6,6 +6,7 @@
 //   a5  level-ordered copy of the triangle + row binning
 // Everything runs in hand-written kernels; the host only sizes allocations.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 
@@ -321,6 +322,85 @@ __global__ void __launch_bounds__(256) k_levels(int n, const int32_t *__restrict
     if (lane == 0 && my_max >= 0) atomicMax(&stat->max_lev, my_max);
 }
 
+// ------------------------------------------------------- a3 (default): Kahn by rounds
+// The paper's analysis (Kahn's topological sort by rounds): the
+// frontier of round l is exactly level l (0-based, reading Q4).  One
+// cooperative kernel walks the rounds with a grid barrier between them
+// instead of one launch per round; a frontier row's dependents
+// (CSC of the referenced strict triangle) get their remaining-dependency
+// counter decremented, and the one that reaches 0 is appended to the next
+// frontier.  No spin-waiting on other rows: the sync-free k_levels above
+// spends ~1 s on cfg4's 12,288 levels (its spinning warps load L2 and its
+// chains serialise inside a warp).  Only lev[] is taken from here; ilev /
+// jlev come from the stable radix sort, so the atomic append order (P:780,
+// P:804) never shows.
+__global__ void k_dep_count(int n, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ colidx, int uplo,
+                            int32_t *cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5)
+        for (int k = rowptr[i] + lane; k < rowptr[i + 1]; k += 32) {
+            const int j = colidx[k];
+            if (in_tri(i, j, uplo)) atomicAdd(&cnt[j], 1);
+        }
+}
+__global__ void k_dep_fill(int n, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ colidx, int uplo,
+                           const int32_t *__restrict__ cptr, int32_t *cur, int32_t *crow) {
+    const int lane = threadIdx.x & 31;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5)
+        for (int k = rowptr[i] + lane; k < rowptr[i + 1]; k += 32) {
+            const int j = colidx[k];
+            if (in_tri(i, j, uplo)) crow[cptr[j] + atomicAdd(&cur[j], 1)] = i;
+        }
+}
+__global__ void k_frontier0(int n, const int32_t *__restrict__ dp, int32_t *F, int32_t *cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && dp[i] == 0) F[atomicAdd(cnt, 1)] = i;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64a(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_barrier_a(unsigned long long *bar, unsigned long long target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+        while (ld_acquire_u64a(bar) < target) {
+        }
+    }
+    __syncthreads();
+}
+constexpr int kKahnThreads = 128;
+__global__ void __launch_bounds__(kKahnThreads) k_kahn(int n, const int32_t *__restrict__ cptr,
+                                                       const int32_t *__restrict__ crow, int32_t *indeg,
+                                                       int32_t *F0, int32_t *F1, int32_t *cnt, int32_t *lev,
+                                                       unsigned long long *bar, AnalysisStatus *stat) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nt = gridDim.x * blockDim.x;
+    // three frontier counters: round l reads cnt[l%3], appends to cnt[(l+1)%3]
+    // and clears cnt[(l+2)%3] (read in round l-1, appended to in round l+1):
+    // one grid barrier per round
+    int l = 0;
+    for (;; ++l) {
+        int32_t *Fc = (l & 1) ? F1 : F0;
+        int32_t *Fn = (l & 1) ? F0 : F1;
+        const int nf = __ldcg(&cnt[l % 3]);
+        if (nf == 0) break;
+        if (tid == 0) cnt[(l + 2) % 3] = 0;
+        for (int idx = tid; idx < nf; idx += nt) {
+            const int i = __ldcg(&Fc[idx]);
+            lev[i] = l;
+            const int k1 = cptr[i + 1];
+            for (int k = cptr[i]; k < k1; ++k) {
+                const int r = crow[k];
+                if (atomicSub(&indeg[r], 1) == 1) Fn[atomicAdd(&cnt[(l + 1) % 3], 1)] = r;
+            }
+        }
+        grid_barrier_a(bar, (unsigned long long)(l + 1) * gridDim.x);
+    }
+    if (tid == 0) stat->max_lev = l - 1;
+}
+
 // ------------------------------------------------------- a4: bucketing
 // ilev from the level-sorted keys: level boundaries (no level is empty).
 __global__ void k_ilev_from_sorted(const uint32_t *skeys, int n, int nlev, int32_t *ilev) {
@@ -504,8 +584,43 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     if ((st = tmp.alloc_n(&d_ticket, 1)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned), s));
     SPTRSV_CUDA(cudaMemsetAsync(h->d_lev, 0xFF, sizeof(int32_t) * (size_t)n, s));
-    k_levels<<<grid_for(((int64_t)n + 31) / 32 * 32, 256, h->num_sms * 8), 256, 0, s>>>(
-        n, rowptr, colidx, h->uplo, h->d_lev, d_ticket, d_stat);
+    const char *esf = getenv("SPTRSV_LEVELS_SYNCFREE");     // 1: the sync-free k_levels
+    if (esf && *esf == '1') {
+        k_levels<<<grid_for(((int64_t)n + 31) / 32 * 32, 256, h->num_sms * 8), 256, 0, s>>>(
+            n, rowptr, colidx, h->uplo, h->d_lev, d_ticket, d_stat);
+    } else {
+        // CSC of the referenced strict triangle (dependents), then Kahn by rounds
+        int32_t *ccnt = nullptr, *cptr = nullptr, *ccur = nullptr, *crow = nullptr, *indeg = nullptr;
+        int32_t *F0 = nullptr, *F1 = nullptr, *fcnt = nullptr;
+        unsigned long long *kbar = nullptr;
+        const int64_t nstrict = (int64_t)hs.used;           // referenced strict entries
+        if ((st = tmp.alloc_n(&ccnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&cptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&ccur, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&crow, (size_t)std::max<int64_t>(nstrict, 1))) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&indeg, (size_t)n)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&F0, (size_t)n)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&F1, (size_t)n)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&fcnt, 3)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&kbar, 1)) != SPTRSV_SUCCESS) return st;
+        SPTRSV_CUDA(cudaMemsetAsync(ccnt, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+        SPTRSV_CUDA(cudaMemsetAsync(ccur, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+        SPTRSV_CUDA(cudaMemsetAsync(fcnt, 0, sizeof(int32_t) * 3, s));
+        SPTRSV_CUDA(cudaMemsetAsync(kbar, 0, sizeof(unsigned long long), s));
+        const int wg = grid_for((int64_t)n * 32, 256, h->num_sms * 16);
+        k_dep_count<<<wg, 256, 0, s>>>(n, rowptr, colidx, h->uplo, ccnt);
+        if ((st = exclusive_scan_i32(ccnt, cptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+        k_dep_fill<<<wg, 256, 0, s>>>(n, rowptr, colidx, h->uplo, cptr, ccur, crow);
+        SPTRSV_CUDA(cudaMemcpyAsync(indeg, h->d_dp, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        k_frontier0<<<(n + 255) / 256, 256, 0, s>>>(n, h->d_dp, F0, fcnt);
+        SPTRSV_CUDA(cudaGetLastError());
+        int per_sm = 0;
+        SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kahn, kKahnThreads, 0));
+        const int kg = std::max(1, std::min(per_sm, 1)) * h->num_sms;
+        void *args[] = {(void *)&n, (void *)&cptr, (void *)&crow, (void *)&indeg, (void *)&F0, (void *)&F1,
+                        (void *)&fcnt, (void *)&h->d_lev, (void *)&kbar, (void *)&d_stat};
+        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_kahn, kg, kKahnThreads, args, 0, s));
+    }
     SPTRSV_CUDA(cudaGetLastError());
     SPTRSV_CUDA(cudaMemcpyAsync(&hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s));
     SPTRSV_CUDA(cudaStreamSynchronize(s));

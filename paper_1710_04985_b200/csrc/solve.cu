@@ -902,7 +902,7 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
             // half the SMs' worth of warps is enough and loads L2 less
             // (cfg3, 13 deps/row: 2.47 -> 2.14 ms; cfg4 26.8 -> 26.6 ms; cfg2,
             // 3 deps/row, prefers 148 CTAs: 0.54 vs 0.62 ms)
-            const int64_t strict = h->info.nnz_used - (h->diag == SPTRSV_NON_UNIT ? (int64_t)h->n : 0);
+            const int64_t strict = h->info.nnz_used;          // referenced strict entries
             if (h->n > 0 && strict >= 8 * (int64_t)h->n) h->self_grid = std::max(1, h->self_grid / 2);
             const char *ec = getenv("SPTRSV_SELF_CPS");      // CTAs per SM (fewer spinning warps)
             if (ec && atoi(ec) > 0) h->self_grid = std::min(h->self_grid, atoi(ec) * h->num_sms);
