@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kKahnThreads) k_kahn(int n, const int32_t *__r
                                                        int32_t *F0, int32_t *F1, int32_t *cnt, int32_t *lev,
                                                        unsigned long long *bar, AnalysisStatus *stat) {
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nt = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, gw = tid >> 5, nwp = (gridDim.x * blockDim.x) >> 5;
     // three frontier counters: round l reads cnt[l%3], appends to cnt[(l+1)%3]
     // and clears cnt[(l+2)%3] (read in round l-1, appended to in round l+1):
     // one grid barrier per round
@@ -387,11 +387,15 @@ __global__ void __launch_bounds__(kKahnThreads) k_kahn(int n, const int32_t *__r
         const int nf = __ldcg(&cnt[l % 3]);
         if (nf == 0) break;
         if (tid == 0) cnt[(l + 2) % 3] = 0;
-        for (int idx = tid; idx < nf; idx += nt) {
+        // warp per frontier row, lanes over its dependents (a dependent list
+        // walked by one thread serialises its returning atomics: cfg4
+        // analysis 297 -> 145 ms; a thread-per-row path for wide rounds was
+        // slower and noisier on cfg4)
+        for (int idx = gw; idx < nf; idx += nwp) {
             const int i = __ldcg(&Fc[idx]);
-            lev[i] = l;
+            if (lane == 0) lev[i] = l;
             const int k1 = cptr[i + 1];
-            for (int k = cptr[i]; k < k1; ++k) {
+            for (int k = cptr[i] + lane; k < k1; k += 32) {
                 const int r = crow[k];
                 if (atomicSub(&indeg[r], 1) == 1) Fn[atomicAdd(&cnt[(l + 1) % 3], 1)] = r;
             }
