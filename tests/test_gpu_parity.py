@@ -540,3 +540,17 @@ def test_multi_rhs_value_as_flag(S, nrhs, uplo, diag, dtype):
     torch.cuda.synchronize()
     assert np.array_equal(Bi.cpu().numpy(), X)
     assert watchdog_clear(S)
+
+
+@pytest.mark.parametrize("uplo", ["lower", "upper"])
+def test_levels_kahn_and_syncfree_agree(S, uplo, monkeypatch):
+    """Both level computations (Kahn by rounds, default; sync-free k_levels,
+    SPTRSV_LEVELS_SYNCFREE=1) give the oracle's levels bit for bit."""
+    m = random_triangular_fast(20000, 6.0, 11, uplo)
+    ref = oracle.analyze(m, uplo, "non_unit")
+    for env in ("0", "1"):
+        monkeypatch.setenv("SPTRSV_LEVELS_SYNCFREE", env)
+        lev, ilev, jlev, nlev = S.from_csr(m, uplo).levels()
+        assert nlev == ref["nlev"]
+        assert np.array_equal(lev, ref["lev"]) and np.array_equal(jlev, ref["jlev"])
+        assert np.array_equal(ilev, ref["ilev"])
