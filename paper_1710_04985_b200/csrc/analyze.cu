@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 
 #include "internal.h"
@@ -538,6 +539,17 @@ static int grid_for(int64_t items, int per_block, int cap) {
 sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
                              const void *vals, cudaStream_t s) {
     const int n = h->n;
+    // SPTRSV_TIMING=1: host wall-clock per analysis phase (stream synchronised) to stderr
+    const bool timing = getenv("SPTRSV_TIMING") && *getenv("SPTRSV_TIMING") == '1';
+    auto tlast = std::chrono::steady_clock::now();
+    auto phase = [&](const char *name) {
+        if (!timing) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[sptrsv analyze] %-10s %8.2f ms\n", name,
+                std::chrono::duration<double, std::milli>(now - tlast).count());
+        tlast = now;
+    };
     DevArena tmp;
     struct Guard {
         DevArena &a;
@@ -582,6 +594,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
         return SPTRSV_ERR_ZERO_PIVOT;
     }
 
+    phase("validate");
     // a3: levels
     if ((st = h->arena.alloc_n(&h->d_lev, n)) != SPTRSV_SUCCESS) return st;
     unsigned *d_ticket = nullptr;
@@ -632,6 +645,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     h->info.nlev = nlev;
     if ((uint64_t)nlev * kBuckets >= (1ull << 32)) return SPTRSV_ERR_NOT_SUPPORTED;
 
+    phase("levels");
     // a4: jlev = rows stably sorted by level; ilev = level boundaries
     uint32_t *keys = nullptr, *skeys = nullptr;
     if ((st = tmp.alloc_n(&keys, n)) != SPTRSV_SUCCESS) return st;
@@ -645,6 +659,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     k_ilev_from_sorted<<<eg, 256, 0, s>>>(skeys, n, nlev, h->d_ilev);
     SPTRSV_CUDA(cudaGetLastError());
 
+    phase("bucket");
     // a5: solve order (level, WPR first, TPR by decreasing deps) and chunks
     if ((st = h->arena.alloc_n(&h->d_perm, n)) != SPTRSV_SUCCESS) return st;
     k_solve_keys<<<eg, 256, 0, s>>>(h->d_lev, h->d_dp, n, keys);
@@ -695,6 +710,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
                                             h->d_ecol, (float *)h->d_eval, (float *)h->d_invd);
     SPTRSV_CUDA(cudaGetLastError());
 
+    phase("layout");
     // synchronisation state
     if ((st = h->arena.alloc_n(&h->d_flags, n)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(h->d_flags, 0, sizeof(int32_t) * (size_t)n, s));
@@ -706,6 +722,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     h->epoch = 0;
     h->bar_base = 0;
 
+    phase("sync");
     // summary
     std::vector<int32_t> il((size_t)nlev + 1);
     SPTRSV_CUDA(cudaMemcpyAsync(il.data(), h->d_ilev, sizeof(int32_t) * il.size(), cudaMemcpyDeviceToHost, s));
@@ -713,6 +730,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     int maxw = 0;
     for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, il[l + 1] - il[l]);
     h->info.max_level_width = maxw;
+    phase("summary");
     return SPTRSV_SUCCESS;
 }
 
