@@ -57,16 +57,16 @@ typedef enum {
     SPTRSV_ALGO_SELF = 0,   /* self-scheduled, per-row ready flags (SLFR) */
     SPTRSV_ALGO_LEVEL = 1,  /* level-scheduled, grid-wide barrier per level (LEVR) */
     SPTRSV_ALGO_BLOCK = 2,  /* self-scheduled over warp-owned row tiles, register/shared-memory
-                               hand-offs (any matrix, fastest on structured grids) */
-    SPTRSV_ALGO_AUTO = 3,   /* BLOCK when the analysis detects a structured grid, else SELF;
+                               hand-offs.  Any matrix on a detected structured
+                               grid; otherwise only if nnz_used <= 3 n (NOT_SUPPORTED above) */
+    SPTRSV_ALGO_AUTO = 3,   /* BLOCK when the analysis detects a structured grid AND every row
+                               has <= 3 dependencies (5-/7-point factors), else SELF;
                                info.algo then reports the algorithm chosen */
-    SPTRSV_ALGO_TILE = 4,   /* CTA tiles: level-synchronous inside a CTA (x in shared memory),
-                               producer-CTA level counters between CTAs;
-                               structured grids with <= 3 dependencies per row */
+    /* 4: retired (round-1 CTA-tile variant); sptrsv_set_algo(4) returns INVALID_VALUE */
     SPTRSV_ALGO_SLFC = 5,   /* column-wise self-scheduled (Alg. SLFC, kernel P:631-653):
                                per-column dependency counters, x updates pushed by L2
                                atomics; last-bit results vary run to run (atomic order).
-                               nrhs > 1 solves use the self-scheduled row kernel */
+                               nrhs > 1 solves use the self-scheduled row kernels */
     SPTRSV_ALGO_LEVC = 6    /* column-wise level-scheduled (Alg. LEVC, kernel
                                P:536-552): atomics, grid-wide barrier per level.  nrhs > 1
                                solves use the level-scheduled row kernel */
@@ -80,7 +80,8 @@ typedef enum {
     SPTRSV_ERR_ALLOC = 4,           /* device or host allocation failed */
     SPTRSV_ERR_CUDA = 5,            /* a CUDA runtime call failed (message via sptrsv_last_cuda_error) */
     SPTRSV_ERR_NOT_SUPPORTED = 6,   /* no sm_100 device, or a size beyond the int32 index space */
-    SPTRSV_ERR_TIMEOUT = 7          /* reserved: spin watchdog (debug builds) */
+    SPTRSV_ERR_TIMEOUT = 7          /* a BLOCK solve gave up a spin wait (watchdog, default 4 s);
+                                       reported by sptrsv_get_solve_status, x is invalid */
 } sptrsv_status_t;
 
 typedef struct {
@@ -128,19 +129,32 @@ sptrsv_status_t sptrsv_analyze(int32_t n, const int32_t *rowptr, const int32_t *
                                sptrsv_handle_t *out);
 
 /*
- * sptrsv_solve -- x = T^{-1} b on `stream`, asynchronous (no host sync).
+ * sptrsv_solve -- x = T^{-1} b on `stream`.
  *   b, x   DEVICE pointers, row-major n x nrhs of the handle's dtype;
  *          x == b (in place, "x is first initialized as f") is allowed;
  *          other overlaps are not.  Caller-owned; valid until the stream
- *          work completes.
- *   nrhs   >= 1.  nrhs == 1 uses the handle's algorithm; nrhs > 1 uses the
- *          multi-RHS self-scheduled kernel (one flag per row, lanes over RHS).
- * Per (row, column) the arithmetic is s = b(i); s -= a(k) * x(ja(k)) as a
- * fused multiply-add in storage order; x(i) = s * (1/d(i)) (or s for UNIT),
- * so results are run-to-run bitwise reproducible and independent of nrhs
- * for the same algorithm.
+ *          work completes.  Alignment: the dtype's natural alignment.
+ *   nrhs   >= 1, any width.  nrhs == 1 uses the handle's algorithm.  nrhs > 1:
+ *          nrhs <= 16 (and algorithm not LEVEL / LEVC) the self-scheduled
+ *          value-as-flag multi-RHS kernel; otherwise the level-scheduled
+ *          multi-RHS kernel over independent column blocks of <= 128.
+ * Arithmetic per (row, column): s = b(i); s = fma(-a(k), x(ja(k)), s) in CSR
+ * storage order; x(i) = s * (1/d(i)) (s for UNIT).  This holds for BLOCK, for
+ * every multi-RHS kernel and for SELF / LEVEL rows with <= 16 dependencies,
+ * so those results are run-to-run bitwise reproducible and a column's result
+ * does not depend on nrhs or the column block it is in.  SELF / LEVEL rows
+ * with > 16 dependencies (warp per row) sum lane partials with a fixed
+ * shuffle tree and compute b(i) - sum (reproducible, not storage order);
+ * SLFC / LEVC accumulate with atomics (order varies run to run).
+ * Asynchrony: no host synchronization, except on the first multi-RHS solve of
+ * a handle, which builds the per-position CSR (allocates, synchronizes
+ * `stream`).  In-place SELF and multi-RHS solves copy b into a handle-owned
+ * scratch buffer (stream-ordered allocation, cudaMallocAsync) because x is
+ * their flag array.  Run one multi-RHS solve before capturing a CUDA graph.
  * Returns INVALID_VALUE on bad arguments, the analysis status if the handle
- * holds an analysis error, CUDA on a launch failure.
+ * holds an analysis error, CUDA on a launch failure.  A BLOCK solve whose spin
+ * wait exceeded the watchdog returns SUCCESS here (it is asynchronous) and
+ * TIMEOUT from sptrsv_get_solve_status.
  */
 sptrsv_status_t sptrsv_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs,
                              sptrsv_stream_t stream);
@@ -173,6 +187,15 @@ sptrsv_status_t sptrsv_get_levels(sptrsv_handle_t h, int32_t *lev, int32_t *ilev
 
 /* Copies the dependency counts dp[n] to a HOST buffer. */
 sptrsv_status_t sptrsv_get_dep_counts(sptrsv_handle_t h, int32_t *dp);
+
+/*
+ * sptrsv_get_solve_status -- synchronizes the device, then reports whether the
+ * LAST solve on the handle completed: SUCCESS, or TIMEOUT if it was a BLOCK
+ * solve that gave up a spin wait (its x is invalid).  The watchdog is per
+ * handle and per solve: the next solve starts clean.  (SPEC.md:259 timeout
+ * guard; the other algorithms have no watchdog and always report SUCCESS.)
+ */
+sptrsv_status_t sptrsv_get_solve_status(sptrsv_handle_t h);
 
 /* Static string for a status code. */
 const char *sptrsv_status_string(sptrsv_status_t s);

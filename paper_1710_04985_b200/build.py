@@ -1,6 +1,11 @@
-"""Build libsptrsv.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+"""Build libsptrsv.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+Each .cu is compiled to an object in parallel (the translation units share no
+device symbols), then linked into one shared library.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import glob
 import os
 import subprocess
@@ -12,13 +17,10 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libsptrsv.so")
+OBJDIR = os.path.join(LIBDIR, "obj")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-diag-suppress", "177",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "177"]
 
 
 def sources():
@@ -31,14 +33,30 @@ def nvcc() -> str:
     return cand if os.path.exists(cand) else "nvcc"
 
 
+def _compile(cu: str, headers_mtime: float, force: bool, verbose: bool) -> str:
+    obj = os.path.join(OBJDIR, os.path.basename(cu)[:-3] + ".o")
+    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(cu), headers_mtime):
+        return obj
+    tmp = obj + f".tmp{os.getpid()}"
+    cmd = [nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-c", "-o", tmp, cu]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    os.replace(tmp, obj)
+    return obj
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(OBJDIR, exist_ok=True)
     srcs = sources()
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
         return LIB
     cu = [s for s in srcs if s.endswith(".cu")]
+    hdr = max(os.path.getmtime(s) for s in srcs if not s.endswith(".cu"))
+    with cf.ThreadPoolExecutor(max_workers=min(8, len(cu))) as ex:
+        objs = list(ex.map(lambda c: _compile(c, hdr, force, verbose), cu))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-o", tmp, *cu]
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

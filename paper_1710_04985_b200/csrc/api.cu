@@ -146,13 +146,11 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
 extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
     if (!h) return SPTRSV_ERR_INVALID_VALUE;
     if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK &&
-        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_TILE && algo != SPTRSV_ALGO_SLFC &&
-        algo != SPTRSV_ALGO_LEVC)
+        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_SLFC && algo != SPTRSV_ALGO_LEVC)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
     // AUTO only uses BLOCK for rows with <= 3 dependencies: skip its build otherwise
-    const bool want_block = algo == SPTRSV_ALGO_BLOCK || algo == SPTRSV_ALGO_TILE ||
-                            (algo == SPTRSV_ALGO_AUTO && h->info.max_row_deps <= 3);
+    const bool want_block = algo == SPTRSV_ALGO_BLOCK || (algo == SPTRSV_ALGO_AUTO && h->info.max_row_deps <= 3);
     if (want_block && !h->block.built && h->n > 0) {
         SPTRSV_CUDA(cudaSetDevice(h->device));
         sptrsv_status_t st = block_build(h, nullptr);
@@ -160,19 +158,13 @@ extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo
         h->info.nblocks = h->block.built ? h->block.nblocks : 0;
         h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
     }
-    if (algo == SPTRSV_ALGO_TILE && !h->tile.built && h->n > 0 &&
-        h->block.built && h->block.grid_nx > 0) {
-        SPTRSV_CUDA(cudaSetDevice(h->device));
-        sptrsv_status_t st = h->block.tm_built ? SPTRSV_SUCCESS : tile_mrhs_build(h, nullptr);
-        if (st == SPTRSV_SUCCESS) st = tile_build(h, nullptr);
-        if (st != SPTRSV_SUCCESS && algo == SPTRSV_ALGO_TILE) return st;
-        h->info.device_bytes = h->arena.bytes + (int64_t)h->stage_bytes;
-    }
-    if (algo == SPTRSV_ALGO_TILE && !h->tile.built) return SPTRSV_ERR_NOT_SUPPORTED;
+    // BLOCK on a natural-order partition (no grid detected) with more than 3
+    // dependencies per row on average: most terms would take the overflow
+    // path (cfg4 measured 75x slower than SELF in round 1) -- refused
+    if (algo == SPTRSV_ALGO_BLOCK && h->n > 0 && h->block.grid_nx == 0 && h->info.nnz_used > 3 * (int64_t)h->n)
+        return SPTRSV_ERR_NOT_SUPPORTED;
     // AUTO: BLOCK on detected grids with <= 3 dependencies per row (5- / 7-point
-    // factors: cfg1 24 us vs 80 us, cfg2 0.27 vs 0.54 ms for SELF); SELF
-    // otherwise (27-point ILU cfg3: SELF 2.89 ms vs BLOCK 3.84 ms;
-    // profiles/bench_cfgs_r1g.json)
+    // factors), SELF otherwise (27-point ILU cfg3, general matrices)
     if (algo == SPTRSV_ALGO_AUTO)
         algo = (h->block.built && h->block.grid_nx > 0 && h->info.max_row_deps <= 3) ? SPTRSV_ALGO_BLOCK
                                                                                       : SPTRSV_ALGO_SELF;
@@ -211,6 +203,15 @@ extern "C" sptrsv_status_t sptrsv_get_dep_counts(sptrsv_handle_t h, int32_t *dp)
     return SPTRSV_SUCCESS;
 }
 
+extern "C" sptrsv_status_t sptrsv_get_solve_status(sptrsv_handle_t h) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) return SPTRSV_SUCCESS;
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    SPTRSV_CUDA(cudaDeviceSynchronize());
+    return block_solve_status(h);
+}
+
 extern "C" const char *sptrsv_status_string(sptrsv_status_t s) {
     switch (s) {
         case SPTRSV_SUCCESS: return "SPTRSV_SUCCESS";
@@ -226,3 +227,34 @@ extern "C" const char *sptrsv_status_string(sptrsv_status_t s) {
 }
 
 extern "C" const char *sptrsv_last_cuda_error(void) { return sptrsv::g_last_cuda; }
+
+// ---------------------------------------------------------------- debug hooks
+// Not part of include/sptrsv.h: test and profiling instrumentation.
+
+// BLOCK spin-watchdog timeout of the handle in ns (default 4e9).  Tests set a
+// tiny value to force SPTRSV_ERR_TIMEOUT.
+extern "C" int sptrsv_dbg_set_timeout_ns(sptrsv_handle_t h, unsigned long long ns) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->timeout_ns = ns;
+    return SPTRSV_SUCCESS;
+}
+
+// Per-warp %globaltimer trace of BLOCK solves: dev_buf holds nunits x cap
+// uint64 (entry t: start of step t, t < cap - 1, at TMA-block starts; entry
+// cap - 1: end).  NULL disables.
+extern "C" int sptrsv_dbg_block_trace(sptrsv_handle_t h, void *dev_buf, int cap) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->block.trace = dev_buf;
+    h->block.trace_cap = dev_buf ? cap : 0;
+    return SPTRSV_SUCCESS;
+}
+
+// BLOCK plan summary for tools: {K, wpc, nsteps, G, nslots, smem, rec_bytes, tile_w, tile_h}
+extern "C" int sptrsv_dbg_block_plan(sptrsv_handle_t h, long long *out9) {
+    if (!h || !out9) return SPTRSV_ERR_INVALID_VALUE;
+    const sptrsv::BlockPlan &B = h->block;
+    const long long v[9] = {B.nblocks, B.wpc, B.nsteps, B.G, B.nslots, (long long)B.smem, B.rec_bytes, B.tile_w,
+                            B.tile_h};
+    for (int i = 0; i < 9; ++i) out9[i] = v[i];
+    return B.built ? SPTRSV_SUCCESS : SPTRSV_ERR_NOT_SUPPORTED;
+}

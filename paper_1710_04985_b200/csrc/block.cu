@@ -1,43 +1,49 @@
-// block.cu -- SPTRSV_ALGO_BLOCK: self-scheduling over warp-owned row tiles with
-// register / shared-memory hand-offs (SURVEY.md §7 hard part H1).
+// block.cu -- SPTRSV_ALGO_BLOCK: self-scheduling over warp-owned row tiles
+// (SURVEY.md §7 hard part H1).
 //
 // Why: the self-scheduled solve's time is its critical path, nlev dependent
-// hand-offs (382 on cfg2).  On B200 a cross-SM hand-off costs one
-// L2 round trip (~220 ns one way, profiles/microbench_r1.json) while a warp
-// shuffle costs ~25 cycles.  So the rows are partitioned over warps such that
-// almost every edge of the critical path stays inside one warp:
+// hand-offs (382 on cfg2).  A cross-SM hand-off costs an L2 round
+// trip (~220 ns one way, profiles/microbench_r1.json), a warp shuffle ~25
+// cycles.  So the rows are partitioned over warps such that almost every edge
+// of the critical path stays inside one warp:
 //
 //   * structured grids (detected: every dependency is verified to be a 3x3x3
 //     neighbour under the inferred nx, ny): a warp owns a tile of <= 32
-//     z-columns (x,y), a CTA a rectangle of warp tiles; lane = column.  Warp
+//     z-columns (x, y), a CTA a rectangle of warp tiles; lane = column.  Warp
 //     step t solves the tile's rows of its t-th level, so the dependencies of
-//     a row on (x-1,y,z), (x,y-1,z), (x,y,z-1) (7-point) were solved in the
-//     previous step by this warp: they arrive by __shfl_sync from registers.
-//   * otherwise contiguous natural-order row blocks (correct for any matrix;
-//     SPTRSV_ALGO_AUTO only picks BLOCK when a grid was detected).
+//     a 7-point row on (x-1,y,z), (x,y-1,z), (x,y,z-1) were solved in the
+//     previous step by this warp and arrive by __shfl_sync from registers.
+//   * otherwise contiguous natural-order row blocks (correct for any matrix).
 //
 // A warp walks its steps in level order (every dependency has a
 // lower level, so the lowest unfinished step can always proceed; all CTAs are
-// co-resident by cooperative launch).  Per dependency, the analysis stores a
-// source code:
+// co-resident by cooperative launch).  Per dependency term the analysis
+// stores a 32-bit code, kind in bits 30-31:
 //   SHFL(l)   solved by this warp in the previous step by lane l: __shfl_sync
-//   SMEM(i)   solved by a warp of this CTA: shared slot i, value-as-flag
-//             (slots prefilled with a NaN sentinel, polled with volatile LDS)
-//   GLOB(g)   solved by another CTA: global mailbox g, value-as-flag polled with
-//             relaxed loads issued one step ahead.  Two mailbox arrays swap
-//             roles every solve (device epoch): each CTA re-arms its own range
-//             of the idle array with the sentinel while it works on the other.
-//   NONE      padding
-// Non-SHFL terms are accumulated first (they are ready early), SHFL terms last,
-// so a step's critical chain is shuffle -> FMAs -> scale.  The order is fixed
-// per row, so results are run-to-run bitwise reproducible (reading Q8).
+//   SMEM(i)   solved by another warp of this CTA: shared slot i (value-as-flag,
+//             slots filled with a NaN sentinel at kernel start, never reused)
+//   GLOB(g)   solved by another CTA: global mailbox g (value-as-flag; two
+//             mailbox arrays swap roles every solve -- device epoch -- and each
+//             CTA re-arms its own range of the idle one)
+//   NONE      padding (payload p > 0: the row's terms are in overflow list p-1)
 //
-// Per (warp, step) the analysis writes one fixed-size record (SoA over lanes)
-//   int32 row | oslot | og | ovf | code[W]  ||  T invd | val[W]
-// streamed into a per-warp shared-memory ring by TMA (cp.async.bulk +
-// mbarrier, nst records in flight); b[row] is gathered PB steps ahead with
-// cp.async into a per-warp ring.  Rows with more than W dependencies keep
-// their entries in an overflow list (codes SMEM/GLOB only, kNone-terminated).
+// Row arithmetic = the paper's sweep with FMAs in STORAGE order:
+//   s = b(i); s = fma(-a_k, x(j_k), s) for k in CSR order; x(i) = s * (1/d(i))
+// -- the same sequence as SELF's thread-per-row rows and every multi-RHS
+// kernel, so results are run-to-run bitwise reproducible and equal across
+// algorithms that share it (reading Q8).
+//
+// One warp per tile does everything; nothing on its per-step critical chain
+// (shuffle -> select -> 3 FMA -> multiply) waits on memory:
+//   records   (codes, coefficients, publish slots) of step t+DR*UB: TMA bulk
+//             copies into a per-warp ring, L2-prefetched DP blocks ahead
+//   row ids   TMA into a per-warp ring DW blocks ahead
+//   b(row)    cp.async gathers into a per-warp ring DBS steps ahead
+//   GLOB EXT  relaxed loads DG steps ahead into a register ring
+//   SMEM EXT  volatile shared loads one step ahead
+// A value still holding the sentinel when its step comes is re-polled (the
+// only wait).  A per-solve watchdog (timeout_ns) turns a hung wait into
+// SPTRSV_ERR_TIMEOUT via sptrsv_get_solve_status instead of a hung GPU.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -48,34 +54,95 @@
 namespace sptrsv {
 namespace {
 
-constexpr int32_t kNone = (int32_t)(3u << 30);
-__host__ __device__ inline int32_t code_smem(int i) { return (int32_t)((1u << 30) | (unsigned)i); }
-__host__ __device__ inline int32_t code_glob(int g) { return (int32_t)((2u << 30) | (unsigned)g); }
+// ---------------------------------------------------------------- term codes
+// A term code is a 32-bit word.  SHFL terms are the source lane itself
+// (0..31), so `code < 32` decides SHFL in one compare and the code is the
+// __shfl_sync lane operand.  Other kinds carry the kind in bits 30-31:
+//   0 with payload 32      NONE (padding term)
+//   0 with payload 33 + o  the row's terms are in overflow list o
+//   2 (SMEM) slot index, 3 (GLOB) mailbox index (< 2^30)
+constexpr unsigned kKNone = 0u, kKSmem = 2u, kKGlob = 3u;
+constexpr int32_t kNoneCode = 32, kOvfBase = 33;
+__host__ __device__ inline int32_t mk_code(unsigned kind, unsigned payload) {
+    return (int32_t)((kind << 30) | (payload & 0x3FFFFFFFu));
+}
 __host__ __device__ inline unsigned code_kind(int32_t c) { return (unsigned)c >> 30; }
 __host__ __device__ inline int code_idx(int32_t c) { return c & 0x3FFFFFFF; }
+__host__ __device__ inline bool code_shfl(int32_t c) { return (unsigned)c < 32u; }
+constexpr int32_t kOvfEnd = -1;          // overflow-list terminator (kind GLOB, payload all ones)
+constexpr int kSH = 3;                   // terms per record row
 
-// Record of one (warp, step), SoA over 32 lanes, every part a multiple of 16 B:
-//   compute part: int4 {row, oslot, og, srcs}[32]          (one LDS.128)
-//                 T {invd, a_0 .. a_SH-1}: (SH+1) values in 16-byte groups [g][32]
-//   helper part:  int ecode[WE][32] | T eval[WE][32]
-//   srcs: bits 0-2 = number of SHFL terms, then 5 bits per source lane.
-//   ecode[0] = kOvf | i: all EXT terms of the row are in the overflow list at i.
-__host__ __device__ constexpr int rec_cv(int) { return 512; }
-__host__ __device__ constexpr int rec_ec(int SH, int es) { return 512 + 32 * es * (SH + 1); }
-__host__ __device__ constexpr int rec_ev(int SH, int WE, int es) { return rec_ec(SH, es) + 128 * WE; }
-__host__ __device__ constexpr int rec_bytes(int SH, int WE, int es) { return rec_ev(SH, WE, es) + 32 * es * WE; }
-constexpr int kSH = 3;                       // SHFL terms per row (compute warp)
-constexpr int32_t kOvfTag = (int32_t)(3u << 30) | (1 << 29);     // kind NONE + bit 29: overflow index
+// ---------------------------------------------------------------- records
+// Two streams per (warp, step), SoA over 32 lanes, 16-byte aligned parts:
+//   ctl  int4 {code0, code1, code2, row}[32]                               512 B
+//        row: -1 on padding lanes
+//   coef T = double: double2 {a0, a1}[32] | double2 {a2, 1/d}[32] | int2 {pub_s, pub_g}[32]   1280 B
+//        T = float : float4 {a0, a1, a2, 1/d}[32] | int2 {pub_s, pub_g}[32]                    768 B
+//        pub_s: shared slot or -1; pub_g: mailbox or -1
+// The control stream is read further ahead (b gathers, GLOB prefetch) than
+// the coefficients, so it has the deeper ring.  Every warp's steps are padded
+// to a multiple of UNR with empty steps (no bounds checks in the loop).
+constexpr int kCtlBytes = 512;
+template <typename T> struct Coef;
+template <> struct Coef<double> {
+    static constexpr int BYTES = 1280, PUB = 1024;
+    double a0, a1, a2, invd;
+    __device__ __forceinline__ void load(const unsigned char *r, int lane) {
+        const double2 c0 = reinterpret_cast<const double2 *>(r)[lane];
+        const double2 c1 = reinterpret_cast<const double2 *>(r + 512)[lane];
+        a0 = c0.x; a1 = c0.y; a2 = c1.x; invd = c1.y;
+    }
+    __device__ static void put(unsigned char *r, int lane, const double (&a)[3], double invd, int2 pub) {
+        reinterpret_cast<double2 *>(r)[lane] = make_double2(a[0], a[1]);
+        reinterpret_cast<double2 *>(r + 512)[lane] = make_double2(a[2], invd);
+        reinterpret_cast<int2 *>(r + PUB)[lane] = pub;
+    }
+};
+template <> struct Coef<float> {
+    static constexpr int BYTES = 768, PUB = 512;
+    float a0, a1, a2, invd;
+    __device__ __forceinline__ void load(const unsigned char *r, int lane) {
+        const float4 c = reinterpret_cast<const float4 *>(r)[lane];
+        a0 = c.x; a1 = c.y; a2 = c.z; invd = c.w;
+    }
+    __device__ static void put(unsigned char *r, int lane, const float (&a)[3], float invd, int2 pub) {
+        reinterpret_cast<float4 *>(r)[lane] = make_float4(a[0], a[1], a[2], invd);
+        reinterpret_cast<int2 *>(r + PUB)[lane] = pub;
+    }
+};
 
 constexpr int kBuckets = kTprMax + 2;
 __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax ? 0u : (uint32_t)(kTprMax + 1 - deps); }
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
+// ---------------------------------------------------------------- pipeline shape
+// b(row) DG steps ahead goes to shared memory by cp.async, one commit group
+// per step, so `cp.async.wait_group DG-1` waits for exactly the oldest step's
+// load (register-ring loads would share counting scoreboards and wait for the
+// newest ones too); b also gets an L2 prefetch PB steps ahead.  Values from
+// other CTAs reach shared slots through the CTA's fetcher warp, so a step
+// only reads shared memory, every load one step before its use (stage
+// registers).
+constexpr int UB = 4;                  // steps per TMA block
+constexpr int NCB = 8, DC = 7;         // control ring (blocks) / TMA lookahead (blocks)
+constexpr int NFB = 4, DF = 3;         // coefficient ring (blocks) / TMA lookahead (blocks)
+constexpr int DP = 12;                 // L2 prefetch lookahead (blocks), both streams
+constexpr int DG = 8;                  // b(row) and GLOB loads in flight (steps): cp.async landing rings
+constexpr int PB = 16;                 // b(row) L2 prefetch distance (steps)
+constexpr int UNR = 8;                 // main-loop unroll = per-warp step padding
+constexpr int XB = (PB + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
+constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
+static_assert(NCB > DC && NFB > DF && UNR % DG == 0 && UNR % UB == 0, "ring shapes");
+static_assert((PB + 1 + UB - 1) / UB + 2 <= DC, "control records must land before their b prefetch");
+static_assert((NCB * UB) % UNR == 0 && (NFB * UB) % UNR == 0, "ring offsets advance by whole iterations");
+
+// per compute warp: control ring, coefficient ring, b landing [DG][32], barriers
+template <typename T>
+__host__ __device__ constexpr size_t warp_smem_bytes() {
+    return ((size_t)NCB * UB * kCtlBytes + (size_t)NFB * UB * Coef<T>::BYTES + (size_t)DG * 32 * sizeof(T) +
+            8 * (NCB + NFB) + 127) / 128 * 128;
 }
 
-// -------------------------------------------------------------- build kernels
+// ---------------------------------------------------------------- build kernels
 // natural-order CSR of the referenced strict triangle, from the chunk layout
 template <typename T>
 __global__ void k_tri_fill(int nchunks, const ChunkDesc *__restrict__ chunks, const int32_t *__restrict__ perm,
@@ -123,14 +190,22 @@ __global__ void k_grid_check(int n, int nx, int ny, const int32_t *__restrict__ 
     if (!ok) atomicAdd(bad, 1u);
 }
 
-// (x, y) tiles of tw x th columns; CTA = wx x wy tiles; unit = cta * wpc + warp
-__global__ void k_part_tiles(int n, int nx, int ny, int tw, int th, int wx, int wy, int cxn, int32_t *unit) {
+// (x, y) tiles of tw x th columns; CTA = wx x wy tiles; unit = cta * wpc + warp.
+// UPPER numbers the CTAs backwards so that every dependency points to a
+// lower-numbered CTA in both cases.
+__global__ void k_part_tiles(int n, int nx, int ny, int tw, int th, int wx, int wy, int cxn, int K, int upper,
+                             int32_t *unit) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int x = i % nx, y = (i / nx) % ny;
     const int txi = x / tw, tyi = y / th;
-    const int cta = (tyi / wy) * cxn + txi / wx;
-    unit[i] = cta * (wx * wy) + (tyi % wy) * wx + (txi % wx);
+    int cta = (tyi / wy) * cxn + txi / wx;
+    int w = (tyi % wy) * wx + (txi % wx);
+    if (upper) {
+        cta = K - 1 - cta;
+        w = wx * wy - 1 - w;
+    }
+    unit[i] = cta * (wx * wy) + w;
 }
 
 __global__ void k_part_natural(int n, int U, int uplo, int32_t *unit) {
@@ -209,34 +284,78 @@ __global__ void k_cta_p0(int K, int wpc, int nsteps, int n, const int32_t *unit_
     cta_p0[c] = s < nsteps ? steps[s].x : n;
 }
 
-// Dependency classes.  Walking a row's dependencies in storage order, the
-// first SH that were solved by the same warp in the previous step are SHFL
-// (the compute warp's registers); the others are EXT, resolved by the helper
-// warp: from a shared slot (producer in the same CTA, bit 0 of need) or from
-// a global mailbox (bit 1).  noslot: that CTA's slots overflowed -> GLOB.
-// ecnt[pos] = number of EXT dependencies of the row at solve position pos.
-__global__ void k_need(int n, int SH, int wpc, const int32_t *__restrict__ tri_ptr,
-                       const int32_t *__restrict__ tri_col, const int32_t *__restrict__ unit,
-                       const int32_t *__restrict__ pos, const int32_t *__restrict__ step_of,
-                       const unsigned char *__restrict__ noslot, int32_t *need, int32_t *ecnt) {
+// Dependency classes: a dependency solved by the same warp in the previous
+// step is SHFL; one solved by another warp of the CTA is read from a shared
+// slot its producer writes (need bit 0); every other one is CROSS: its
+// producer publishes it to a global mailbox (bit 1) and the consumer CTA's
+// fetcher copies it into a shared slot (GLOB in the GL fallback).  noslot:
+// that CTA's slots overflowed -> its intra-CTA dependencies are CROSS too.
+// icnt[pos]: CROSS dependencies of the row at solve position pos.
+__device__ __forceinline__ bool dep_shfl(int ui, int si, int uj, int sj) { return uj == ui && sj == si - 1; }
+__global__ void k_need(int n, int wpc, const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
+                       const int32_t *__restrict__ unit, const int32_t *__restrict__ pos,
+                       const int32_t *__restrict__ step_of, const unsigned char *__restrict__ noslot, int32_t *need,
+                       int32_t *icnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) icnt[n] = 0;
     if (i >= n) return;
-    const int a = tri_ptr[i], e = tri_ptr[i + 1];
-    const int ui = unit[i], si = step_of[pos[i]];
+    const int ui = unit[i], pi = pos[i], si = step_of[pi];
     const bool ns = noslot[ui / wpc] != 0;
-    int nsh = 0, next = 0;
-    for (int k = a; k < e; ++k) {
+    int cross = 0;
+    for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k) {
         const int j = tri_col[k];
         const int uj = unit[j], pj = pos[j];
-        if (nsh < SH && uj == ui && step_of[pj] == si - 1) {
-            ++nsh;
-            continue;
+        if (dep_shfl(ui, si, uj, step_of[pj])) continue;
+        if (uj / wpc == ui / wpc && !ns) {
+            atomicOr(&need[pj], 1);
+        } else {
+            atomicOr(&need[pj], 2);
+            ++cross;
         }
-        ++next;
-        if (uj / wpc == ui / wpc && !ns) atomicOr(&need[pj], 1);
-        else atomicOr(&need[pj], 2);
     }
-    ecnt[pos[i]] = next;
+    icnt[pi] = cross;
+}
+
+// inbound items of CROSS dependencies, numbered by (position, storage order):
+// key (consumer CTA, level), source mailbox
+__global__ void k_items(int n, int nlev, int wpc, const int32_t *__restrict__ bperm, const int32_t *__restrict__ tri_ptr,
+                        const int32_t *__restrict__ tri_col, const int32_t *__restrict__ unit,
+                        const int32_t *__restrict__ pos, const int32_t *__restrict__ step_of,
+                        const int32_t *__restrict__ lev, const int32_t *__restrict__ g_scan,
+                        const int32_t *__restrict__ iptr, uint32_t *key, int32_t *mb) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int i = bperm[p];
+    const int ui = unit[i], si = step_of[p];
+    int q = iptr[p];
+    const uint32_t kk = (uint32_t)(ui / wpc) * (uint32_t)nlev + (uint32_t)lev[i];
+    for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k) {
+        const int j = tri_col[k];
+        const int uj = unit[j], pj = pos[j];
+        if (dep_shfl(ui, si, uj, step_of[pj]) || uj / wpc == ui / wpc) continue;   // (no noslot CTA here)
+        key[q] = kk;
+        mb[q] = g_scan[pj];
+        ++q;
+    }
+}
+
+__global__ void k_cta_iptr(int K, const int32_t *cta_p0, const int32_t *iptr, int32_t *fptr) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= K) fptr[c] = iptr[cta_p0[c]];
+}
+
+// sorted item q -> fetcher entry {mailbox, slot}; slot of every item (after the CTA's intra slots)
+__global__ void k_item_place(int nitems, int K, int nlev, const uint32_t *iskey, const int32_t *iperm,
+                             const int32_t *imb, const int32_t *slot_scan, const int32_t *cta_p0,
+                             const int32_t *fptr, int2 *fitems, int32_t *islot) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nitems) return;
+    const int c = (int)(iskey[q] / (uint32_t)nlev);
+    const int intra = slot_scan[cta_p0[c + 1]] - slot_scan[cta_p0[c]];
+    const int slot = intra + (q - fptr[c]);
+    const int item = iperm[q];
+    fitems[q] = make_int2(imb[item], slot);
+    islot[item] = slot;
 }
 
 __global__ void k_need_bits(int n, const int32_t *need, int bit, int32_t *out) {
@@ -245,90 +364,115 @@ __global__ void k_need_bits(int n, const int32_t *need, int bit, int32_t *out) {
     if (p == n) out[p] = 0;
 }
 
-__global__ void k_ovf_count(int n, int WE, const int32_t *ecnt, int32_t *cnt) {
+// overflow-list length by position: rows with more than kSH terms (+ terminator)
+__global__ void k_ovf_count(int n, const int32_t *bperm, const int32_t *dp, int32_t *cnt) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) cnt[p] = ecnt[p] > WE ? ecnt[p] + 1 : 0;       // + terminator
+    if (p < n) {
+        const int d = dp[bperm[p]];
+        cnt[p] = d > kSH ? d + 1 : 0;
+    }
     if (p == n) cnt[p] = 0;
 }
 
-// per CTA: number of shared slots it needs
-__global__ void k_cta_slots(int K, const int32_t *cta_p0, const int32_t *slot_scan, int32_t *cnt) {
+// per CTA: number of shared slots it needs (intra-CTA, + inbound if iptr)
+__global__ void k_cta_slots(int K, const int32_t *cta_p0, const int32_t *slot_scan, const int32_t *iptr, int32_t *cnt) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < K) cnt[c] = slot_scan[cta_p0[c + 1]] - slot_scan[cta_p0[c]];
+    if (c < K)
+        cnt[c] = slot_scan[cta_p0[c + 1]] - slot_scan[cta_p0[c]] + (iptr ? iptr[cta_p0[c + 1]] - iptr[cta_p0[c]] : 0);
 }
 
-// one thread per (step, lane): the record of that lane (padding lanes included)
+// mailbox range of every CTA
+__global__ void k_cta_g0(int K, const int32_t *cta_p0, const int32_t *g_scan, int32_t *g0) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c <= K) g0[c] = g_scan[cta_p0[c]];
+}
+
+// every record of both streams = an empty step (all lanes padding)
 template <typename T>
-__global__ void k_rec_fill(int nsteps, int SH, int WE, int wpc, const int2 *__restrict__ steps,
+__global__ void k_pad_fill(int64_t nrec, unsigned char *__restrict__ ctl, unsigned char *__restrict__ coef) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nrec * 32) return;
+    const int s = (int)(t >> 5), lane = (int)(t & 31);
+    reinterpret_cast<int4 *>(ctl + (size_t)s * kCtlBytes)[lane] = make_int4(kNoneCode, kNoneCode, kNoneCode, -1);
+    const T a[kSH] = {T(0), T(0), T(0)};
+    Coef<T>::put(coef + (size_t)s * Coef<T>::BYTES, lane, a, T(0), make_int2(-1, -1));
+}
+
+// padded step index of every step: warp u's steps start at pstart[u]
+__global__ void k_pad_map(int nsteps, const int32_t *step_unit, const int32_t *unit_step0, const int32_t *pstart,
+                          int32_t *pmap) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsteps) return;
+    const int u = step_unit[s];
+    pmap[s] = pstart[u] + (s - unit_step0[u]);
+}
+
+__global__ void k_pad_count(int U, const int32_t *unit_step0, int32_t *cnt) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < U) cnt[u] = (unit_step0[u + 1] - unit_step0[u] + UNR - 1) / UNR * UNR;
+    if (u == U) cnt[u] = 0;
+}
+
+// one thread per (step, lane): that lane's entries of both streams, at the
+// step's padded position
+template <typename T>
+__global__ void k_rec_fill(int nsteps, int wpc, const int2 *__restrict__ steps, const int32_t *__restrict__ pmap,
                            const int32_t *__restrict__ bperm, const int32_t *__restrict__ pos,
                            const int32_t *__restrict__ step_of, const int32_t *__restrict__ unit,
                            const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
                            const T *__restrict__ tri_val, const T *__restrict__ invd_row, int unit_diag,
                            const unsigned char *__restrict__ noslot, const int32_t *__restrict__ need,
-                           const int32_t *__restrict__ ecnt, const int32_t *__restrict__ slot_scan,
-                           const int32_t *__restrict__ g_scan, const int32_t *__restrict__ cta_p0,
-                           const int32_t *__restrict__ ovf_ptr, unsigned char *__restrict__ recs,
-                           int32_t *__restrict__ rows, int32_t *__restrict__ ovf_code, T *__restrict__ ovf_val) {
+                           const int32_t *__restrict__ slot_scan, const int32_t *__restrict__ g_scan,
+                           const int32_t *__restrict__ cta_p0, const int32_t *__restrict__ ovf_ptr,
+                           const int32_t *__restrict__ iptr, const int32_t *__restrict__ islot, int gl,
+                           unsigned char *__restrict__ ctl, unsigned char *__restrict__ coef,
+                           int32_t *__restrict__ ovf_code, T *__restrict__ ovf_val) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (long long)nsteps * 32) return;
     const int s = (int)(t >> 5), lane = (int)(t & 31);
-    const int es = (int)sizeof(T), G16 = 16 / es;
-    rows[t] = lane < steps[s].y ? bperm[steps[s].x + lane] : -1;            // values per 16-byte group
-    unsigned char *base = recs + (size_t)s * rec_bytes(SH, WE, es);
-    int4 *ci = reinterpret_cast<int4 *>(base);
-    T *cv = reinterpret_cast<T *>(base + rec_cv(SH));
-    int32_t *ec = reinterpret_cast<int32_t *>(base + rec_ec(SH, es));
-    T *ev = reinterpret_cast<T *>(base + rec_ev(SH, WE, es));
-    auto cvp = [&](int q) -> T & { return cv[((q / G16) * 32 + lane) * G16 + (q % G16)]; };
     const int2 st = steps[s];
-    for (int q = 0; q <= SH; ++q) cvp(q) = T(0);
-    for (int q = 0; q < WE; ++q) {
-        ec[q * 32 + lane] = kNone;
-        ev[q * 32 + lane] = T(0);
-    }
-    if (lane >= st.y) {
-        ci[lane] = make_int4(-1, -1, -1, 0);
-        return;
-    }
+    if (lane >= st.y) return;                       // padding lane: k_pad_fill's empty entry stays
+    const size_t ps = (size_t)pmap[s];
+    unsigned char *cr = ctl + ps * kCtlBytes;
+    unsigned char *fr = coef + ps * Coef<T>::BYTES;
+    T a[kSH] = {T(0), T(0), T(0)};
     const int p = st.x + lane;
     const int i = bperm[p];
     const int ui = unit[i], cta = ui / wpc;
     const bool ns = noslot[cta] != 0;
-    const int nd = need[p];
     const int si = step_of[p];
-    const int a = tri_ptr[i], e = tri_ptr[i + 1];
-    const bool ovf = ecnt[p] > WE;
-    int srcs = 0, nsh = 0, ne = 0;
+    const int ka = tri_ptr[i], ke = tri_ptr[i + 1];
+    const int slot_base = slot_scan[cta_p0[cta]];
+    int32_t code[kSH] = {kNoneCode, kNoneCode, kNoneCode};
+    const bool ovf = ke - ka > kSH;
     int o = ovf ? ovf_ptr[p] : 0;
-    if (ovf) ec[lane] = kOvfTag | o;
-    for (int k = a; k < e; ++k) {
+    if (ovf) code[0] = kOvfBase + o;
+    int item = gl ? 0 : iptr[p];
+    for (int k = ka, q = 0; k < ke; ++k, ++q) {
         const int j = tri_col[k];
         const int uj = unit[j], pj = pos[j];
-        if (nsh < SH && uj == ui && step_of[pj] == si - 1) {
-            srcs |= (pj - steps[si - 1].x) << (3 + 5 * nsh);
-            cvp(1 + nsh) = tri_val[k];
-            ++nsh;
-            continue;
-        }
-        const int32_t c = (uj / wpc == cta && !ns) ? code_smem(slot_scan[pj] - slot_scan[cta_p0[cta]])
-                                                   : code_glob(g_scan[pj]);
+        int32_t c;
+        if (dep_shfl(ui, si, uj, step_of[pj])) c = pj - steps[si - 1].x;                  // SHFL: source lane
+        else if (uj / wpc == cta && !ns) c = mk_code(kKSmem, (unsigned)(slot_scan[pj] - slot_base));
+        else if (gl) c = mk_code(kKGlob, (unsigned)g_scan[pj]);
+        else c = mk_code(kKSmem, (unsigned)islot[item++]);                                // inbound slot
         if (ovf) {
             ovf_code[o] = c;
             ovf_val[o] = tri_val[k];
             ++o;
         } else {
-            ec[ne * 32 + lane] = c;
-            ev[ne * 32 + lane] = tri_val[k];
-            ++ne;
+            code[q] = c;
+            a[q] = tri_val[k];
         }
     }
     if (ovf) {
-        ovf_code[o] = kNone;
+        ovf_code[o] = kOvfEnd;
         ovf_val[o] = T(0);
     }
-    cvp(0) = unit_diag ? T(1) : invd_row[i];
-    ci[lane] = make_int4(i, (nd & 1) ? slot_scan[p] - slot_scan[cta_p0[cta]] : -1, (nd & 2) ? g_scan[p] : -1,
-                         srcs | nsh);
+    const int nd = need[p];
+    reinterpret_cast<int4 *>(cr)[lane] = make_int4(code[0], code[1], code[2], i);
+    Coef<T>::put(fr, lane, a, unit_diag ? T(1) : invd_row[i],
+                 make_int2((nd & 1) ? slot_scan[p] - slot_base : -1, (nd & 2) ? g_scan[p] : -1));
 }
 
 template <typename T>
@@ -339,6 +483,11 @@ __global__ void k_fill_sentinel(T *p, int64_t n) {
 }
 
 // ------------------------------------------------------------------ solve
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ double lds_volatile(const double *p) {
     double v;
     asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
@@ -349,78 +498,7 @@ __device__ __forceinline__ float lds_volatile(const float *p) {
     asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
     return v;
 }
-__device__ __forceinline__ void sts_volatile(double *p, double v) {
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v) : "memory");
-}
-__device__ __forceinline__ void sts_volatile(float *p, float v) {
-    asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
-}
-__device__ __forceinline__ void cp_async_val(double *dst, const double *src) { cp_async_8(dst, src); }
-__device__ __forceinline__ void cp_async_val(float *dst, const float *src) { cp_async_4(dst, src); }
-
-// Spin watchdog: a wait that exceeds ~4 s (a scheduling bug, never expected
-// on valid input) sets g_watchdog and gives up instead of hanging the GPU.
-__device__ unsigned g_watchdog = 0;
-__device__ __forceinline__ unsigned long long wd_now() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-__device__ __noinline__ bool wd_expired(unsigned long long t0) {
-    if (*(volatile unsigned *)&g_watchdog) return true;      // another wait already gave up
-    if (wd_now() - t0 > 4000000000ull) {
-        atomicExch(&g_watchdog, 1u);
-        return true;
-    }
-    return false;
-}
-
-template <typename T>
-__device__ __noinline__ T poll_smem_slow(const T *p) {
-    const unsigned long long t0 = wd_now();
-    T v = lds_volatile(p);
-    unsigned it = 0;
-    while (Sentinel<T>::is(v)) {
-        if (++it > 64) __nanosleep(32);
-        v = lds_volatile(p);
-        if ((it & 1023u) == 0 && wd_expired(t0)) break;
-    }
-    return v;
-}
-template <typename T>
-__device__ __noinline__ T poll_global_slow(const T *p) {
-    const unsigned long long t0 = wd_now();
-    T v = ld_relaxed_val(p);
-    unsigned it = 0;
-    while (Sentinel<T>::is(v)) {
-        if (++it > 16) __nanosleep(64);
-        v = ld_relaxed_val(p);
-        if ((it & 1023u) == 0 && wd_expired(t0)) break;
-    }
-    return v;
-}
-
-// Debug-only timeline hook (sptrsv_dbg_block_trace): lane 0 of every warp
-// records %globaltimer at its first `cap` - 1 steps and at the end.
-__device__ unsigned long long *g_trace = nullptr;
-__device__ int g_trace_cap = 0;
-__device__ unsigned long long *g_phase = nullptr;   // warp 0: 6 clock64 stamps x 128 steps
-
-struct BlockArgs {
-    const int32_t *unit_step0;
-    const unsigned char *recs;
-    const int32_t *rows;          // [nsteps][32] row of every lane (-1: padding)
-    const int32_t *cta_g0;
-    const int32_t *ovf_code;
-    const void *ovf_val;
-    void *gmb;
-    unsigned *ctr;
-    const void *b;
-    void *x;
-    int G, nslots;
-};
-
-// predicated value-as-flag loads (no branch: returns 0 where !pred)
+// predicated value-as-flag loads (return 0 where !pred)
 __device__ __forceinline__ double ldg_flag_if(const double *p, bool pred) {
     unsigned long long v = 0;
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.gpu.global.b64 %0, [%1];\n\t}"
@@ -451,683 +529,433 @@ __device__ __forceinline__ void sts_flag(double *p, double v) {
 __device__ __forceinline__ void sts_flag(float *p, float v) {
     asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
 }
-// store ordered after every earlier memory access of the thread (compiler side)
-__device__ __forceinline__ void sts_flag_last(double *p, double v) {
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v) : "memory");
-}
-__device__ __forceinline__ void sts_flag_last(float *p, float v) {
-    asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
-}
 __device__ __forceinline__ void stg_flag(double *p, double v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v)));
 }
 __device__ __forceinline__ void stg_flag(float *p, float v) {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(__float_as_uint(v)));
 }
-__device__ __forceinline__ void cp_async_wait_n(int n) {      // n <= 7
-    switch (n) {
-        case 0: cp_async_wait<0>(); break;
-        case 1: cp_async_wait<1>(); break;
-        case 2: cp_async_wait<2>(); break;
-        case 3: cp_async_wait<3>(); break;
-        case 4: cp_async_wait<4>(); break;
-        case 5: cp_async_wait<5>(); break;
-        case 6: cp_async_wait<6>(); break;
-        default: cp_async_wait<7>(); break;
-    }
-}
-
-// the SH + 1 record values {invd, a_0 .. a_SH-1} of one lane (16-byte groups)
-template <typename T> struct CV;
-template <> struct CV<double> {
-    double v[4];
-    __device__ __forceinline__ void load(const unsigned char *p, int lane) {
-        const double2 g0 = reinterpret_cast<const double2 *>(p)[lane];
-        const double2 g1 = reinterpret_cast<const double2 *>(p + 512)[lane];
-        v[0] = g0.x; v[1] = g0.y; v[2] = g1.x; v[3] = g1.y;
-    }
-};
-template <> struct CV<float> {
-    float v[4];
-    __device__ __forceinline__ void load(const unsigned char *p, int lane) {
-        const float4 g0 = reinterpret_cast<const float4 *>(p)[lane];
-        v[0] = g0.x; v[1] = g0.y; v[2] = g0.z; v[3] = g0.w;
-    }
-};
-static_assert(kSH == 3, "CV<T> holds invd + 3 SHFL coefficients");
-
-// predicated cp.async of one value (no branch; nothing copied where !pred)
-__device__ __forceinline__ void cp_async_val_if(double *dst, const double *src, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 8;\n\t}" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"((unsigned)pred)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_val_if(float *dst, const float *src, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"((unsigned)pred)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_wd(uint64_t *bar, uint32_t ph) {
-    if (!mbar_try_wait(bar, ph)) {
-        const unsigned long long t0 = wd_now();
-        while (!mbar_try_wait(bar, ph))
-            if (wd_expired(t0)) break;
-    }
-}
-
-// Warp-specialised tile solve.  A CTA owns ntw tiles; tile w has a COMPUTE
-// warp (warp w) and a HELPER warp (warp ntw + w).  The helper works in blocks
-// of UB steps:
-//   records   block k+DB by one TMA bulk copy (ring of NBB blocks, mbarrier per slot)
-//   row ids   block k+R1B by one TMA bulk copy (ring of RRB blocks)
-//   b[row]    block k+R2B by cp.async, one group per block
-//   EXT terms of the block's UB steps: all their loads issued first (shared
-//             slots / global mailboxes, value-as-flag), then per step
-//             c = b - sum_EXT a x (storage order) -> the step's c slot
-//             (value-as-flag: the NaN sentinel while empty)
-// The compute warp, per step: waits for its lane's c, x = (c - sum_SHFL a
-// x_prev) * invd with the SHFL sources shuffled from the previous step's
-// results, stores x (and the shared slot / mailbox copies other warps need)
-// and re-arms the c slot.  Its critical chain between two levels is shuffle
-// -> FMA chain -> multiply.  The helper runs at most (NBB - DB) blocks ahead:
-// record slot k+DB reuses the slot of block k+DB-NBB, free once the compute
-// warp re-armed the c slot of that block's last step.
-constexpr int kDB = 3, kNBB = 5, kR2B = 2, kBR = 4, kR1B = 4, kRRB = 4, kPFB = 12;   // kBR: 2 helpers x 2 blocks of b
-__host__ __device__ constexpr int ub_of(int WE) { return WE <= 4 ? 4 : 2; }   // steps per helper block
-template <typename T, bool UNIT, int WE>
-__global__ void __launch_bounds__(384, 1) k_block(const BlockArgs a) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    __shared__ unsigned s_epoch;
-    constexpr int SH = kSH, UB = ub_of(WE), DB = kDB, NBB = kNBB, R2B = kR2B, R1B = kR1B, RRB = kRRB;
-    constexpr int ES = (int)sizeof(T);
-    constexpr int REC = rec_bytes(SH, WE, ES);
-    constexpr int CVO = rec_cv(SH), ECO = rec_ec(SH, ES), EVO = rec_ev(SH, WE, ES);
-    constexpr int NCS = NBB * UB;                 // c ring (steps)
-    constexpr size_t TILE = ((size_t)NBB * UB * REC + (size_t)RRB * UB * 128 + (size_t)NCS * 32 * ES +
-                             (size_t)kBR * UB * 32 * ES + 8 * (NBB + RRB) + 127) / 128 * 128;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ntw = blockDim.x / 96;              // tiles per CTA: 1 compute + 2 helper warps each
-    const int w = warp % ntw;
-    const bool helper = warp >= ntw;
-    const int hid = helper ? (warp - ntw) / ntw : 0;   // helper 0 takes even blocks, helper 1 odd
-    unsigned char *tb = smem_raw + (size_t)w * TILE;
-    unsigned char *ring = tb;                                        // [NBB*UB][REC]
-    int32_t *rw = reinterpret_cast<int32_t *>(tb + (size_t)NBB * UB * REC);      // [RRB*UB][32]
-    T *cr = reinterpret_cast<T *>(rw + RRB * UB * 32);              // [NCS][32]
-    T *br = cr + NCS * 32;                                           // [kBR*UB][32]
-    uint64_t *recbar = reinterpret_cast<uint64_t *>(br + kBR * UB * 32);
-    uint64_t *rowbar = recbar + NBB;
-    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)ntw * TILE);
-    const T *b = static_cast<const T *>(a.b);
-    T *x = static_cast<T *>(a.x);
-
-    for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
-    if (helper && hid == 0) {
-        for (int i = lane; i < NCS * 32; i += 32) cr[i] = Sentinel<T>::value();
-        if (lane == 0) {
-            for (int i = 0; i < NBB + RRB; ++i) mbar_init(&recbar[i], 1);
-            fence_mbar_init();
-        }
-    }
-    if (threadIdx.x == 0) s_epoch = (unsigned)ld_relaxed(reinterpret_cast<const int *>(a.ctr));
-    __syncthreads();
-    const unsigned par = s_epoch & 1u;
-    T *gm = static_cast<T *>(a.gmb) + (size_t)par * a.G;
-    {   // re-arm this CTA's mailboxes of the idle array (written by the previous solve)
-        T *go = static_cast<T *>(a.gmb) + (size_t)(par ^ 1u) * a.G;
-        for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
-            go[i] = Sentinel<T>::value();
-    }
-
-    const int u = blockIdx.x * ntw + w;
-    const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;
-    if (n > 0 && helper) {
-        const int nblk = (n + UB - 1) / UB;
-        const unsigned char *grec = a.recs + (size_t)s0 * REC;
-        const int32_t *grow = a.rows + (size_t)s0 * 32;
-        const bool trace = g_trace != nullptr && hid == 0;
-        T *bh = br + hid * 2 * UB * 32;          // this helper's b ring: its blocks k (slot) and k+2
-        auto issue_rec = [&](int kk) {          // lane 0: TMA of record block kk
-            const int slot = kk % NBB;
-            mbar_arrive_expect_tx(&recbar[slot], UB * REC);
-            bulk_g2s(ring + (size_t)slot * UB * REC, grec + (size_t)kk * UB * REC, UB * REC, &recbar[slot]);
-        };
-        auto issue_rows = [&](int kk) {
-            const int slot = kk % RRB;
-            mbar_arrive_expect_tx(&rowbar[slot], UB * 128);
-            bulk_g2s(rw + slot * UB * 32, grow + (size_t)kk * UB * 32, UB * 128, &rowbar[slot]);
-        };
-        auto prefetch_l2 = [&](int kk) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grec + (size_t)kk * UB * REC), "r"(UB * REC)
-                         : "memory");
-        };
-        auto rec_wait = [&](int kk) { mbar_wait_wd(&recbar[kk % NBB], (uint32_t)((kk / NBB) & 1)); };
-        auto issue_b = [&](int kk, int bslot) {  // b of block kk (row ids landed)
-            mbar_wait_wd(&rowbar[kk % RRB], (uint32_t)((kk / RRB) & 1));
-            const int32_t *rr = rw + (kk % RRB) * UB * 32 + lane;
-            T *bb = bh + bslot * UB * 32 + lane;
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const int r = rr[j * 32];
-                cp_async_val_if(bb + j * 32, b + r, r >= 0);
-            }
-        };
-        int32_t ncode[UB][WE];
-        T nv[UB][WE];
-        auto ext_loads = [&](int kk) {           // EXT values of block kk (records landed)
-            const unsigned char *rb = ring + (size_t)(kk % NBB) * UB * REC;
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const int32_t *ec = reinterpret_cast<const int32_t *>(rb + j * REC + ECO) + lane;
-                const bool vj = kk * UB + j < n;          // the last block may hold the next warp's steps
-#pragma unroll
-                for (int q = 0; q < WE; ++q) {
-                    ncode[j][q] = ec[q * 32];
-                    const unsigned kind = code_kind(ncode[j][q]);
-                    const T vs_ = lds_flag_if(slots + code_idx(ncode[j][q]), vj && kind == 1u);
-                    const T vg_ = ldg_flag_if(gm + code_idx(ncode[j][q]), vj && kind == 2u);
-                    nv[j][q] = kind == 1u ? vs_ : vg_;
-                }
-            }
-        };
-        if (hid == 0 && lane == 0) {
-            for (int kk = 0; kk < min(nblk, kPFB); ++kk) prefetch_l2(kk);
-            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk);
-            for (int kk = 0; kk < min(nblk, R1B); ++kk) issue_rows(kk);
-        }
-        if (hid < nblk) {
-            issue_b(hid, 0);
-            cp_async_commit();
-            rec_wait(hid);
-            __syncwarp();
-            ext_loads(hid);
-        }
-#pragma unroll 1
-        for (int k = hid, i = 0; k < nblk; k += 2, ++i) {
-            if (trace && lane == 0 && k * UB < g_trace_cap - 1) g_trace[(size_t)u * g_trace_cap + k * UB] = wd_now();
-            // (1) refill: records k+DB (the slot of block k+DB-NBB, released by the
-            // compute warp), rows k+R1B, L2 prefetch
-            if (k + DB < nblk) {
-                if (k + DB >= NBB) {
-                    const T *f = cr + (((k + DB - NBB) * UB + UB - 1) % NCS) * 32 + lane;
-                    if (__any_sync(0xffffffffu, !Sentinel<T>::is(lds_volatile(f)))) {
-                        const unsigned long long t0 = wd_now();
-                        unsigned it = 0;
-                        while (__any_sync(0xffffffffu, !Sentinel<T>::is(lds_volatile(f)))) {
-                            __nanosleep(20);
-                            if ((++it & 1023u) == 0 && wd_expired(t0)) break;
-                        }
-                    }
-                }
-                if (lane == 0) issue_rec(k + DB);
-            }
-            if (lane == 0) {
-                if (k + R1B < nblk) issue_rows(k + R1B);
-                if (k + kPFB < nblk) prefetch_l2(k + kPFB);
-            }
-            // (2) b of this helper's next block k+2
-            if (k + 2 < nblk) issue_b(k + 2, (i + 1) & 1);
-            cp_async_commit();
-            // (3) block k: b (this helper's previous group) and records
-            cp_async_wait<1>();
-            rec_wait(k);
-            __syncwarp();
-            const unsigned char *rb = ring + (size_t)(k % NBB) * UB * REC;
-            int32_t code[UB][WE];
-            T v[UB][WE];
-#pragma unroll
-            for (int j = 0; j < UB; ++j)
-#pragma unroll
-                for (int q = 0; q < WE; ++q) {
-                    code[j][q] = ncode[j][q];
-                    v[j][q] = nv[j][q];
-                }
-            // (4) EXT loads of this helper's next block k+2 (two blocks of slack)
-            if (k + 2 < nblk) {
-                rec_wait(k + 2);
-                __syncwarp();
-                ext_loads(k + 2);
-            }
-            const int cs = (k * UB) % NCS;
-            const int bs = i & 1;
-            // (5) block k's c values.  Fast path (every EXT value arrived, no
-            // overflow row): straight-line over the UB steps.  Otherwise one step
-            // at a time, publishing each c as soon as its values are there (a
-            // later step of the block may depend on this warp's own results),
-            // re-issuing all pending loads of the block together per round trip.
-            bool pend = false, ovf = false;
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-#pragma unroll
-                for (int q = 0; q < WE; ++q) pend |= Sentinel<T>::is(v[j][q]);
-                ovf |= ((unsigned)code[j][0] & 0xE0000000u) == 0xE0000000u && k * UB + j < n;
-            }
-            const T *evb = reinterpret_cast<const T *>(rb + EVO) + lane;
-            if (!__any_sync(0xffffffffu, pend || ovf)) {
-#pragma unroll
-                for (int j = 0; j < UB; ++j) {
-                    T c = bh[(bs * UB + j) * 32 + lane];
-#pragma unroll
-                    for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
-                    sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < UB; ++j) {
-                    if (k * UB + j >= n) break;
-                    bool pj = false;
-#pragma unroll
-                    for (int q = 0; q < WE; ++q) pj |= Sentinel<T>::is(v[j][q]);
-                    if (__any_sync(0xffffffffu, pj)) {
-                        const unsigned long long t0 = wd_now();
-                        unsigned it = 0;
-                        do {
-#pragma unroll
-                            for (int jj = j; jj < UB; ++jj)
-#pragma unroll
-                                for (int q = 0; q < WE; ++q) {
-                                    const bool p = Sentinel<T>::is(v[jj][q]);
-                                    const unsigned kind = code_kind(code[jj][q]);
-                                    const T vs_ = lds_flag_if(slots + code_idx(code[jj][q]), p && kind == 1u);
-                                    const T vg_ = ldg_flag_if(gm + code_idx(code[jj][q]), p && kind == 2u);
-                                    v[jj][q] = p ? (kind == 1u ? vs_ : vg_) : v[jj][q];
-                                }
-                            pj = false;
-#pragma unroll
-                            for (int q = 0; q < WE; ++q) pj |= Sentinel<T>::is(v[j][q]);
-                            if ((++it & 255u) == 0 && wd_expired(t0)) break;
-                        } while (__any_sync(0xffffffffu, pj));
-                    }
-                    T c = bh[(bs * UB + j) * 32 + lane];
-#pragma unroll
-                    for (int q = 0; q < WE; ++q) c = fnma(evb[j * (REC / ES) + q * 32], v[j][q], c);
-                    if (((unsigned)code[j][0] & 0xE0000000u) == 0xE0000000u) {          // overflow list
-                        const T *ov = static_cast<const T *>(a.ovf_val);
-                        for (int o = code[j][0] & 0x1FFFFFFF;; ++o) {
-                            const int32_t cc = a.ovf_code[o];
-                            if (cc == kNone) break;
-                            T vv;
-                            if (code_kind(cc) == 1u) {
-                                vv = lds_volatile(slots + code_idx(cc));
-                                if (Sentinel<T>::is(vv)) vv = poll_smem_slow(slots + code_idx(cc));
-                            } else {
-                                vv = ld_relaxed_val(gm + code_idx(cc));
-                                if (Sentinel<T>::is(vv)) vv = poll_global_slow(gm + code_idx(cc));
-                            }
-                            c = fnma(ov[o], vv, c);
-                        }
-                    }
-                    sts_flag(cr + (cs + j) * 32 + lane, Sentinel<T>::scrub(c));
-                }
-            }
-        }
-        cp_async_wait<0>();
-        if (trace && lane == 0) g_trace[(size_t)u * g_trace_cap + g_trace_cap - 1] = wd_now();
-    } else if (n > 0) {
-        // software-pipelined: the next step's c and record fields are loaded
-        // before this step's shuffle -> FMA chain; the readiness check of the
-        // next c comes after it (warp-uniform; fields reloaded if it was late)
-        T xprev = T(0);
-        auto wait_c = [&](T *cp) -> T {
-            T c = lds_volatile(cp);
-            if (__any_sync(0xffffffffu, Sentinel<T>::is(c))) {
-                const unsigned long long t0 = wd_now();
-                unsigned it = 0;
-                do {
-                    if (++it > 4) __nanosleep(20);          // leave the issue slots to the helper
-                    c = lds_volatile(cp);
-                    if ((it & 4095u) == 0 && wd_expired(t0)) break;
-                } while (__any_sync(0xffffffffu, Sentinel<T>::is(c)));
-            }
-            return c;
-        };
-        T *cp = cr + lane;
-        T c = wait_c(cp);
-        asm volatile("" ::: "memory");
-        const unsigned char *r = ring;
-        int4 ci = reinterpret_cast<const int4 *>(r)[lane];
-        CV<T> cv;
-        cv.load(r + CVO, lane);
-        int slot = 0;
-#pragma unroll 1
-        for (int t = 0; t < n; ++t) {
-            const int slot1 = slot + 1 == NCS ? 0 : slot + 1;
-            T *cp1 = cr + slot1 * 32 + lane;
-            const unsigned char *r1 = ring + (size_t)slot1 * REC;
-            T c1 = T(0);
-            int4 ci1 = make_int4(-1, -1, -1, 0);
-            CV<T> cv1;
-            const bool more = t + 1 < n;
-            if (more) {
-                c1 = lds_volatile(cp1);
-                asm volatile("" ::: "memory");
-                ci1 = reinterpret_cast<const int4 *>(r1)[lane];
-                cv1.load(r1 + CVO, lane);
-            }
-            const int nsh = ci.w & 7;
-            T acc = c;
-#pragma unroll
-            for (int q = 0; q < SH; ++q) {
-                const T vq = __shfl_sync(0xffffffffu, xprev, (ci.w >> (3 + 5 * q)) & 31);
-                acc = fnma(cv.v[1 + q], q < nsh ? vq : T(0), acc);
-            }
-            const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * cv.v[0];   // (a product is never the sentinel)
-            if (ci.x >= 0) __stcg(x + ci.x, xi);
-            if (ci.y >= 0) sts_flag(slots + ci.y, xi);
-            if (ci.z >= 0) stg_flag(gm + ci.z, xi);
-            sts_flag_last(cr + slot * 32 + lane, Sentinel<T>::value());     // step consumed: re-arm the c slot
-            xprev = xi;
-            if (more && __any_sync(0xffffffffu, Sentinel<T>::is(c1))) {     // the next c was not ready yet
-                c1 = wait_c(cp1);
-                asm volatile("" ::: "memory");
-                ci1 = reinterpret_cast<const int4 *>(r1)[lane];
-                cv1.load(r1 + CVO, lane);
-            }
-            c = c1;
-            ci = ci1;
-            cv = cv1;
-            slot = slot1;
-        }
-    }
-
-    __syncthreads();
-    if (threadIdx.x == 0) {      // the last CTA to finish advances the mailbox epoch
-        __threadfence();
-        if (atomicAdd(&a.ctr[1], 1u) == gridDim.x - 1) {
-            atomicExch(&a.ctr[1], 0u);
-            __threadfence();
-            atomicAdd(&a.ctr[0], 1u);
-        }
-    }
-}
-
-// ---------------------------------------------------------------- lean BLOCK
-// k_block1: the same records, ONE warp per tile doing everything (no helper
-// warp, no c hand-off between warps).  Per step t the warp
-//   (1) loads step t+1's record fields and its SMEM EXT values (shared slots
-//       written by other warps of the CTA, value-as-flag),
-//   (2) solves step t: readiness vote, c = b - sum_EXT a x (storage order),
-//       the SHFL chain, x * invd, stores,
-//   (3) issues step t+2's b[row] and GLOB EXT loads (relaxed) into registers:
-//       two steps of cover for an L2 round trip, so a consumer tile needs to
-//       lag its producer by only ~2 levels (a whole-block prefetch forced
-//       4-7 levels per CTA crossing, tools/wave_trace.py).
-// Per block of kLUB steps: record block k+kLDB by TMA (lane 0), L2 prefetch
-// of records kLPF blocks ahead and of b[row] of block k+2 (records landed).
-// A value still holding the sentinel is re-polled with two loads in flight
-// (half the round trip of overshoot instead of a whole one).  Arithmetic
-// order equals k_block's (bitwise-equal x).
-constexpr int kLUB = 4, kLDB = 3, kLNBB = kLDB + 2, kLPF = 12, kLPB = 4;
-__host__ __device__ constexpr size_t lean_tile_bytes_c(int REC, int) {
-    return ((size_t)kLNBB * kLUB * REC + 8 * kLNBB + 127) / 128 * 128;
-}
-
-template <typename T, int WE>
-struct LState {
-    int4 ci;
-    CV<T> cv;
-    int32_t code[WE];
-    T ev[WE];
-    T v[WE];              // SMEM EXT values (0 for other kinds)
-};
-
-// overflow list of one row (rows with more EXT terms than WE): slow path
+// base + idx (idx < 2^30 elements): one IMAD.WIDE.U32
 template <typename T>
-__device__ __noinline__ T lean_ovf(T c, int o, const int32_t *__restrict__ ovf_code, const T *__restrict__ ovf_val,
-                                   const T *slots, const T *gm) {
-    for (;; ++o) {
-        const int32_t cc = ovf_code[o];
-        if (cc == kNone) break;
-        T vv;
-        if (code_kind(cc) == 1u) {
-            vv = lds_volatile(slots + code_idx(cc));
-            if (Sentinel<T>::is(vv)) vv = poll_smem_slow(slots + code_idx(cc));
-        } else {
-            vv = ld_relaxed_val(gm + code_idx(cc));
-            if (Sentinel<T>::is(vv)) vv = poll_global_slow(gm + code_idx(cc));
-        }
-        c = fnma(ovf_val[o], vv, c);
-    }
-    return c;
+__device__ __forceinline__ T *elem(T *base, int32_t code) {
+    T *r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"((unsigned)code & 0x3FFFFFFFu), "r"((unsigned)sizeof(T)), "l"(base));
+    return r;
 }
 
-__device__ __forceinline__ double ldg_nc_if(const double *p, bool pred) {
-    double v = 0.0;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.f64 %0, [%1];\n\t}"
+// predicated loads merging into v (v unchanged where !pred)
+__device__ __forceinline__ void ldg_flag_into(double &v, const double *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.gpu.global.f64 %0, [%1];\n\t}"
                  : "+d"(v) : "l"(p), "r"((unsigned)pred));
-    return v;
 }
-__device__ __forceinline__ float ldg_nc_if(const float *p, bool pred) {
-    float v = 0.f;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.L1::no_allocate.f32 %0, [%1];\n\t}"
+__device__ __forceinline__ void ldg_flag_into(float &v, const float *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.gpu.global.f32 %0, [%1];\n\t}"
                  : "+f"(v) : "l"(p), "r"((unsigned)pred));
-    return v;
 }
+__device__ __forceinline__ void lds_flag_into(double &v, const double *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.f64 %0, [%1];\n\t}"
+                 : "+d"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
+}
+__device__ __forceinline__ void lds_flag_into(float &v, const float *p, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.f32 %0, [%1];\n\t}"
+                 : "+f"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
+}
+__device__ __forceinline__ unsigned hi_word(double v) { return (unsigned)((unsigned long long)__double_as_longlong(v) >> 32); }
+__device__ __forceinline__ unsigned hi_word(float v) { return __float_as_uint(v); }
+template <typename T> __device__ __forceinline__ unsigned sent_hi();
+template <> __device__ __forceinline__ unsigned sent_hi<double>() { return (unsigned)(Sentinel<double>::bits >> 32); }
+template <> __device__ __forceinline__ unsigned sent_hi<float>() { return Sentinel<float>::bits; }
+
+// the sentinel test on the high word only (finite values and arithmetic NaNs
+// never carry the sentinel's high word)
+__device__ __forceinline__ bool is_sent(double v) {
+    return (unsigned)(__double_as_longlong(v) >> 32) == (unsigned)(Sentinel<double>::bits >> 32);
+}
+__device__ __forceinline__ bool is_sent(float v) { return Sentinel<float>::is(v); }
+
+struct BlockArgs {
+    const int32_t *unit_step0;    // [U+1] padded first step of every warp (multiples of UNR)
+    const unsigned char *ctl;     // control stream [npad + kPadSteps][kCtlBytes]
+    const unsigned char *coef;    // coefficient stream [npad + kPadSteps][Coef<T>::BYTES]
+    const int32_t *cta_g0;        // [K+1] mailbox range of every CTA (values it publishes)
+    const int2 *fitems;           // inbound items {mailbox, shared slot}, by (CTA, level)
+    const int32_t *fptr;          // [K+1] inbound item range of every CTA
+    const int32_t *ovf_code;
+    const void *ovf_val;
+    void *gmb;                    // [2][G] mailboxes
+    unsigned *ctr;                // [0] solve epoch, [1] finished CTAs
+    unsigned *status;             // [0] epoch + 1 of the last solve that timed out
+    unsigned long long *trace;    // debug: per-warp %globaltimer at block starts (NULL: off)
+    int trace_cap;
+    const void *b;
+    void *x;
+    int G, nslots;
+    unsigned long long timeout_ns;
+};
+
+// Watchdog of one wait: true once this solve is given up (this wait exceeded
+// timeout_ns, or another one already did).
+struct Watch {
+    unsigned long long t0;
+    unsigned it;
+    __device__ bool expired(unsigned *status, unsigned long long timeout_ns, unsigned tag) {
+        if ((++it & 255u) != 0) return false;
+        if (it == 256u) t0 = gtimer();
+        if (ld_relaxed(reinterpret_cast<const int *>(status)) == (int)tag) return true;
+        if (gtimer() - t0 > timeout_ns) {
+            st_relaxed(reinterpret_cast<int *>(status), (int)tag);
+            return true;
+        }
+        return false;
+    }
+};
+
 __device__ __forceinline__ void prefetch_l2_if(const void *p, bool pred) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q prefetch.global.L2 [%0];\n\t}" ::"l"(p),
                  "r"((unsigned)pred));
 }
+// predicated stores (no branch in the step body)
+__device__ __forceinline__ void stx_if(double *p, double v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
+                 "r"((unsigned)pred));
+}
+__device__ __forceinline__ void stx_if(float *p, float v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f32 [%0], %1;\n\t}" ::"l"(p), "f"(v),
+                 "r"((unsigned)pred));
+}
+__device__ __forceinline__ void stg_flag_if(double *p, double v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f64 [%0], %1;\n\t}" ::"l"(p),
+                 "d"(v), "r"((unsigned)pred));
+}
+__device__ __forceinline__ void stg_flag_if(float *p, float v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f32 [%0], %1;\n\t}" ::"l"(p),
+                 "f"(v), "r"((unsigned)pred));
+}
+__device__ __forceinline__ void sts_flag_if(double *p, double v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.f64 [%0], %1;\n\t}" ::"r"(
+                     smem_u32(p)), "d"(v), "r"((unsigned)pred));
+}
+__device__ __forceinline__ void sts_flag_if(float *p, float v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.f32 [%0], %1;\n\t}" ::"r"(
+                     smem_u32(p)), "f"(v), "r"((unsigned)pred));
+}
+// cp.async with a source size: 0 zero-fills the destination without reading
+__device__ __forceinline__ void cp_async_val_z(double *dst, const double *src, bool full) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(full ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_val_z(float *dst, const float *src, bool full) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(full ? 4 : 0)
+                 : "memory");
+}
+// TMA bulk copy issued by one lane (predicate), no branch
+__device__ __forceinline__ void tma_if(void *dst, const void *src, uint32_t bytes, uint64_t *bar, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+        "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+        "@q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "r"((unsigned)pred)
+        : "memory");
+}
+__device__ __forceinline__ void l2pf_if(const void *src, uint32_t bytes, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(
+                     src), "r"(bytes), "r"((unsigned)pred)
+                 : "memory");
+}
 
-template <typename T, bool UNIT, int WE>
-__global__ void __launch_bounds__(128, 1) k_block1(const BlockArgs a) {
+// EXT value of one term: shared slot (SMEM) or, in the GL instance only, the
+// mailbox itself (GLOB, polled directly); 0 for other kinds
+template <typename T, bool GL>
+__device__ __forceinline__ T ext_load(int32_t c, const T *slots, const T *gm) {
+    T v = T(0);
+    lds_flag_into(v, slots + code_idx(c), code_kind(c) == kKSmem);
+    if (GL) ldg_flag_into(v, elem(gm, c), code_kind(c) == kKGlob);
+    return v;
+}
+
+// Re-poll the EXT values of a step that are still the sentinel (warp-uniform
+// loop; out of line: the common case never gets here).  By value: nothing of
+// the caller's state becomes addressable.
+template <typename T> struct E3 { T e0, e1, e2; };
+template <typename T, bool GL>
+__device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const T *slots, const T *gm, unsigned *status,
+                                     unsigned long long tmo, unsigned tag) {
+    Watch wd{0, 0};
+    for (;;) {
+        const bool p0 = is_sent(e.e0), p1 = is_sent(e.e1), p2 = is_sent(e.e2);
+        if (!__any_sync(0xffffffffu, p0 || p1 || p2) || wd.expired(status, tmo, tag)) break;
+        if (p0) e.e0 = ext_load<T, GL>(c0, slots, gm);
+        if (p1) e.e1 = ext_load<T, GL>(c1, slots, gm);
+        if (p2) e.e2 = ext_load<T, GL>(c2, slots, gm);
+    }
+    return e;
+}
+
+// overflow row (> kSH terms): warp-uniform walk of the lists of the lanes
+// that have one, in storage order, polling SMEM / GLOB values
+template <typename T>
+__device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const int32_t *oc, const T *ov, const T *slots,
+                                    const T *gm, unsigned *status, unsigned long long tmo, unsigned tag) {
+    for (;;) {
+        const int32_t c = o >= 0 ? oc[o] : kOvfEnd;
+        const bool live = c != kOvfEnd;
+        if (!__any_sync(0xffffffffu, live)) break;
+        const T sh = __shfl_sync(0xffffffffu, xprev, c & 31);
+        if (live) {
+            const unsigned k = code_shfl(c) ? kKNone : code_kind(c);
+            T v = sh;
+            if (k == kKSmem || k == kKGlob) {
+                Watch w{0, 0};
+                for (;;) {
+                    v = k == kKSmem ? lds_volatile(slots + code_idx(c)) : ld_relaxed_val(elem(gm, c));
+                    if (!is_sent(v) || w.expired(status, tmo, tag)) break;
+                }
+            }
+            acc = fnma(ov[o], v, acc);
+            ++o;
+        }
+    }
+    return acc;
+}
+
+// The fetcher (last warp of a CTA): copies the CTA's inbound values (written
+// to global mailboxes by other CTAs) into their shared slots, in the order
+// the CTA's steps need them.  Lane l owns items l, l+32, ...; it keeps kFw of
+// them polled at once (relaxed loads) and moves on once all kFw arrived.
+constexpr int kFw = 4;
+template <typename T>
+__device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
+                        unsigned long long tmo, unsigned tag) {
+    const int lane = threadIdx.x & 31;
+    Watch wd{0, 0};
+    for (int m = f0 + lane; __any_sync(0xffffffffu, m < f1); m += 32 * kFw) {
+        int2 d[kFw];
+        unsigned todo = 0;
+#pragma unroll
+        for (int k = 0; k < kFw; ++k) {
+            const int i = m + 32 * k;
+            d[k] = i < f1 ? items[i] : make_int2(0, 0);
+            if (i < f1) todo |= 1u << k;
+        }
+        while (__any_sync(0xffffffffu, todo != 0)) {
+            T v[kFw];
+#pragma unroll
+            for (int k = 0; k < kFw; ++k) v[k] = (todo >> k) & 1u ? ld_relaxed_val(gm + d[k].x) : T(0);
+            bool got = false;
+#pragma unroll
+            for (int k = 0; k < kFw; ++k)
+                if (((todo >> k) & 1u) && !is_sent(v[k])) {
+                    sts_flag_if(slots + d[k].y, v[k], true);
+                    todo &= ~(1u << k);
+                    got = true;
+                }
+            if (!__any_sync(0xffffffffu, got)) {
+                __nanosleep(64);
+                if (wd.expired(status, tmo, tag)) return;
+            }
+        }
+    }
+}
+
+// Record fields of one step (loaded two steps before the step runs)
+template <typename T>
+struct Stage {
+    int4 c;          // term codes, row
+    int2 pub;        // shared slot, mailbox
+    Coef<T> f;
+};
+
+// OVF: the plan has rows with more than kSH terms (overflow lists).  GL: the
+// plan keeps GLOB terms (mailboxes polled by the consumer itself: shared
+// slots did not fit); otherwise every cross-CTA value reaches its consumer
+// through the CTA's fetcher warp and a shared slot.  The common instance
+// (no OVF, no GL) carries no code for either.
+template <typename T, bool UNIT, bool OVF, bool GL>
+__global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
-    constexpr int SH = kSH, UB = kLUB, DB = kLDB, NBB = kLNBB;
-    constexpr int ES = (int)sizeof(T);
-    constexpr int REC = rec_bytes(SH, WE, ES);
-    constexpr int CVO = rec_cv(SH), ECO = rec_ec(SH, ES), EVO = rec_ev(SH, WE, ES);
-    constexpr size_t TILE = lean_tile_bytes_c(REC, ES);
-    static_assert(UB % 2 == 0 && UB >= 2, "ping-pong state needs an even block length");
+    constexpr int CB = Coef<T>::BYTES;
+    constexpr int CR = NCB * UB, FR = NFB * UB;      // ring lengths (steps), powers of two
+    static_assert((CR & (CR - 1)) == 0 && (FR & (FR - 1)) == 0, "power-of-two rings");
+    constexpr size_t WS = warp_smem_bytes<T>();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ntw = blockDim.x >> 5;
-    unsigned char *tb = smem_raw + (size_t)w * TILE;
-    unsigned char *ring = tb;                                                       // [NBB][UB][REC]
-    uint64_t *recbar = reinterpret_cast<uint64_t *>(tb + (size_t)NBB * UB * REC);
-    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)ntw * TILE);
+    const int wpc = (blockDim.x >> 5) - 1;            // compute warps; warp wpc is the fetcher
+    unsigned char *ctlring = smem_raw + (size_t)w * WS;                                // [CR][kCtlBytes]
+    unsigned char *coefring = ctlring + (size_t)CR * kCtlBytes;                         // [FR][CB]
+    T *bland = reinterpret_cast<T *>(coefring + (size_t)FR * CB);                      // [DG][32]
+    uint64_t *cbar = reinterpret_cast<uint64_t *>(bland + DG * 32);                     // [NCB]
+    uint64_t *fbar = cbar + NCB;                                                        // [NFB]
+    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)wpc * WS);
     const T *b = static_cast<const T *>(a.b);
     T *x = static_cast<T *>(a.x);
 
     for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
-    if (lane == 0) {
-        for (int i = 0; i < NBB; ++i) mbar_init(&recbar[i], 1);
+    if (lane == 0 && w < wpc) {
+        for (int i = 0; i < NCB + NFB; ++i) mbar_init(&cbar[i], 1);
         fence_mbar_init();
     }
     if (threadIdx.x == 0) s_epoch = (unsigned)ld_relaxed(reinterpret_cast<const int *>(a.ctr));
     __syncthreads();
-    const unsigned par = s_epoch & 1u;
-    T *gm = static_cast<T *>(a.gmb) + (size_t)par * a.G;
+    const unsigned epoch = s_epoch;
+    const unsigned tag = epoch + 1u;
+    T *gm = static_cast<T *>(a.gmb) + (size_t)(epoch & 1u) * a.G;
     {   // re-arm this CTA's mailboxes of the idle array (written by the previous solve)
-        T *go = static_cast<T *>(a.gmb) + (size_t)(par ^ 1u) * a.G;
+        T *go = static_cast<T *>(a.gmb) + (size_t)((epoch & 1u) ^ 1u) * a.G;
         for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
             go[i] = Sentinel<T>::value();
     }
+    unsigned *status = a.status;
+    const unsigned long long tmo = a.timeout_ns;
 
-    const int u = blockIdx.x * ntw + w;
-    const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;
+    if (w == wpc) {
+        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, status, tmo, tag);
+    } else {
+    const int u = blockIdx.x * wpc + w;
+    const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;    // n: a multiple of UNR
     if (n > 0) {
-        const int nblk = (n + UB - 1) / UB;
-        const unsigned char *grec = a.recs + (size_t)s0 * REC;
-        unsigned long long *trc = g_trace != nullptr ? g_trace + (size_t)u * g_trace_cap : nullptr;
-        long long dbg[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // debug trace only (g_trace set): cycle counters
-        auto issue_rec = [&](int kk) {
-            const int slot = kk % NBB;
-            mbar_arrive_expect_tx(&recbar[slot], UB * REC);
-            bulk_g2s(ring + (size_t)slot * UB * REC, grec + (size_t)kk * UB * REC, UB * REC, &recbar[slot]);
+        const int nbx = n / UB + XB;             // blocks staged: this warp's + lookahead past its end
+        const unsigned char *gctl = a.ctl + (size_t)s0 * kCtlBytes;
+        const unsigned char *gcoef = a.coef + (size_t)s0 * CB;
+        unsigned long long *trc = a.trace != nullptr ? a.trace + (size_t)u * a.trace_cap : nullptr;
+        const bool l0 = lane == 0;
+        auto issue = [&](int kb) {              // lane 0: TMA of both streams' blocks kb+DC / kb+DF, L2 prefetch
+            const int kc = kb + DC, kf = kb + DF, kp = kb + DP;
+            tma_if(ctlring + (size_t)(kc % NCB) * UB * kCtlBytes, gctl + (size_t)kc * UB * kCtlBytes,
+                   UB * kCtlBytes, &cbar[kc % NCB], l0 && kc >= 0 && kc < nbx);
+            tma_if(coefring + (size_t)((kf + NFB) % NFB) * UB * CB, gcoef + (size_t)kf * UB * CB, UB * CB,
+                   &fbar[(kf + NFB) % NFB], l0 && kf >= 0 && kf < nbx);
+            l2pf_if(gctl + (size_t)kp * UB * kCtlBytes, UB * kCtlBytes, l0 && kp >= DP && kp < nbx);
+            l2pf_if(gcoef + (size_t)kp * UB * CB, UB * CB, l0 && kp >= DP && kp < nbx);
         };
-        auto prefetch_rec = [&](int kk) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grec + (size_t)kk * UB * REC), "r"(UB * REC)
-                         : "memory");
+        auto wait_bar = [&](uint64_t *bar, uint32_t ph) {
+            Watch wd{0, 0};
+            while (!mbar_try_wait(bar, ph))
+                if (wd.expired(status, tmo, tag)) break;
         };
-        auto rec_wait = [&](int kk) { mbar_wait_wd(&recbar[kk % NBB], (uint32_t)((kk / NBB) & 1)); };
-        // b[row] is L2-prefetched kLPB-1 blocks ahead from row ids loaded one block earlier
-        const int32_t *grow = a.rows + (size_t)s0 * 32 + lane;
-        int32_t rowreg[UB];
-        auto load_rows = [&](int kk) {
-#pragma unroll
-            for (int j = 0; j < UB; ++j) rowreg[j] = kk < nblk ? __ldg(grow + ((size_t)kk * UB + j) * 32) : -1;
+        auto try_ctl = [&](int kb) { return kb >= nbx || mbar_try_wait(&cbar[kb % NCB], (uint32_t)((kb / NCB) & 1)); };
+        auto try_coef = [&](int kb) { return kb >= nbx || mbar_try_wait(&fbar[kb % NFB], (uint32_t)((kb / NFB) & 1)); };
+        auto wait_ctl = [&](int kb) { if (kb < nbx) wait_bar(&cbar[kb % NCB], (uint32_t)((kb / NCB) & 1)); };
+        auto wait_coef = [&](int kb) { if (kb < nbx) wait_bar(&fbar[kb % NFB], (uint32_t)((kb / NFB) & 1)); };
+        auto ctl_at = [&](int t) -> int4 {
+            return reinterpret_cast<const int4 *>(ctlring + (size_t)(t & (CR - 1)) * kCtlBytes)[lane];
         };
-        auto prefetch_b = [&]() {
-#pragma unroll
-            for (int j = 0; j < UB; ++j) prefetch_l2_if(b + rowreg[j], rowreg[j] >= 0);
+        auto load_stage = [&](int t, Stage<T> &S) {
+            S.c = ctl_at(t);
+            const unsigned char *fr = coefring + (size_t)(t & (FR - 1)) * CB;
+            S.f.load(fr, lane);
+            S.pub = reinterpret_cast<const int2 *>(fr + Coef<T>::PUB)[lane];
         };
-        // start of block kb: refill the record ring, b prefetch
-        auto block_work = [&](int kb) {
-            const long long c0 = trc != nullptr ? clock64() : 0;
-            __syncwarp();
-            if (lane == 0) {
-                if (kb + DB < nblk) issue_rec(kb + DB);
-                if (kb + kLPF < nblk) prefetch_rec(kb + kLPF);
-            }
-            prefetch_b();                        // b of block kb + kLPB - 1
-            load_rows(kb + kLPB);
-            if (kb + 1 < nblk) rec_wait(kb + 1);
-            if (trc != nullptr) dbg[4] += clock64() - c0;
+        auto load_ext = [&](const Stage<T> &S, E3<T> &E) {
+            E.e0 = ext_load<T, GL>(S.c.x, slots, gm);
+            E.e1 = ext_load<T, GL>(S.c.y, slots, gm);
+            E.e2 = ext_load<T, GL>(S.c.z, slots, gm);
         };
-        auto load_state = [&](LState<T, WE> &S, const unsigned char *r) {
-            S.ci = reinterpret_cast<const int4 *>(r)[lane];
-            S.cv.load(r + CVO, lane);
-#pragma unroll
-            for (int q = 0; q < WE; ++q) {
-                S.code[q] = reinterpret_cast<const int32_t *>(r + ECO)[q * 32 + lane];
-                S.ev[q] = reinterpret_cast<const T *>(r + EVO)[q * 32 + lane];
-                S.v[q] = lds_flag_if(slots + code_idx(S.code[q]), code_kind(S.code[q]) == 1u);
-            }
-        };
-        // b and GLOB EXT values of a step, loads in flight until first use
-        T Bv[2], Gv[2][WE];
-        auto issue_far = [&](int par2, const unsigned char *r, bool valid) {
-            const int row = reinterpret_cast<const int4 *>(r)[lane].x;
-            Bv[par2] = ldg_nc_if(b + row, valid && row >= 0);
-#pragma unroll
-            for (int q = 0; q < WE; ++q) {
-                const int32_t cd = reinterpret_cast<const int32_t *>(r + ECO)[q * 32 + lane];
-                Gv[par2][q] = ldg_flag_if(gm + code_idx(cd), valid && code_kind(cd) == 2u);
-            }
+        // cp.async of b(row) of step t (control entry c), one commit group per step
+        auto far_load = [&](int t, int4 c) {
+            cp_async_val_z(bland + (t & (DG - 1)) * 32 + lane, elem(b, c.w), c.w >= 0);
+            cp_async_commit();
         };
 
-        if (lane == 0) {
-            for (int kk = 0; kk < min(nblk, kLPF); ++kk) prefetch_rec(kk);
-            for (int kk = 0; kk < min(nblk, DB); ++kk) issue_rec(kk);
-        }
-        for (int kk = 0; kk < kLPB - 1; ++kk) {
-            load_rows(kk);
-            prefetch_b();
-        }
-        load_rows(kLPB - 1);
-        rec_wait(0);
-        issue_far(0, ring, true);
-        issue_far(1, ring + REC, n > 1);
-        block_work(0);
-
-        LState<T, WE> st[2];
-        load_state(st[0], ring);
-        T xprev = T(0);
-        int rslot = 0;
-        // one block of UB steps; false when the warp's steps are done
-        auto do_block = [&](int k) -> bool {
-            if (trc != nullptr && lane == 0 && k * UB < g_trace_cap - 16) trc[k * UB] = wd_now();
-            const unsigned char *rbk = ring + (size_t)rslot * UB * REC;
-            const int rslot1 = rslot + 1 == NBB ? 0 : rslot + 1;
-            const unsigned char *rbk1 = ring + (size_t)rslot1 * UB * REC;
-#pragma unroll
-            for (int j = 0; j < UB; ++j) {
-                const int t = k * UB + j;
-                if (t >= n) return false;
-                LState<T, WE> &S = st[j & 1];
-                LState<T, WE> &N = st[(j + 1) & 1];
-                const bool more = t + 1 < n;
-                if (more) {
-                    if (j == UB - 1) {
-                        block_work(k + 1);
-                        load_state(N, rbk1);
-                    } else {
-                        load_state(N, rbk + (size_t)(j + 1) * REC);
-                    }
-                }
-                // EXT readiness (value-as-flag); slow path re-polls with two loads in flight
-                T v[WE];
-                bool pend = false;
-#pragma unroll
-                for (int q = 0; q < WE; ++q) {
-                    const unsigned kind = code_kind(S.code[q]);
-                    v[q] = kind == 2u ? Gv[j & 1][q] : S.v[q];
-                    pend |= (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
-                }
-                if (__any_sync(0xffffffffu, pend)) {
-                    const unsigned long long t0 = wd_now();
-                    const long long c0 = trc != nullptr ? clock64() : 0;
-                    unsigned it = 0;
-                    T inf[WE];
-                    auto issue_polls = [&](T (&dst)[WE]) {
-#pragma unroll
-                        for (int q = 0; q < WE; ++q) {
-                            const unsigned kind = code_kind(S.code[q]);
-                            const bool p = (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
-                            const T vs_ = lds_flag_if(slots + code_idx(S.code[q]), p && kind == 1u);
-                            const T vg_ = ldg_flag_if(gm + code_idx(S.code[q]), p && kind == 2u);
-                            dst[q] = kind == 1u ? vs_ : vg_;
-                        }
-                    };
-                    issue_polls(inf);
-                    do {
-                        T nx[WE];
-                        __nanosleep(32);
-                        issue_polls(nx);
-                        pend = false;
-#pragma unroll
-                        for (int q = 0; q < WE; ++q) {
-                            const unsigned kind = code_kind(S.code[q]);
-                            const bool p = (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
-                            v[q] = (p && !Sentinel<T>::is(inf[q])) ? inf[q] : v[q];
-                            pend |= (kind == 1u || kind == 2u) && Sentinel<T>::is(v[q]);
-                            inf[q] = nx[q];
-                        }
-                        if ((++it & 255u) == 0 && wd_expired(t0)) break;
-                    } while (__any_sync(0xffffffffu, pend));
-                    if (trc != nullptr) {
-                        bool gl = false;
-#pragma unroll
-                        for (int q = 0; q < WE; ++q) gl |= code_kind(S.code[q]) == 2u;
-                        gl = __any_sync(0xffffffffu, gl);
-                        if (t == 0) dbg[0] += clock64() - c0;
-                        else if (gl) { dbg[1] += clock64() - c0; ++dbg[2]; }
-                        else { dbg[3] += clock64() - c0; ++dbg[7]; }
-                    }
-                }
-                T c = Bv[j & 1];
-#pragma unroll
-                for (int q = 0; q < WE; ++q) c = fnma(S.ev[q], v[q], c);
-                if (((unsigned)S.code[0] & 0xE0000000u) == 0xE0000000u && S.ci.x >= 0)
-                    c = lean_ovf<T>(c, S.code[0] & 0x1FFFFFFF, a.ovf_code, static_cast<const T *>(a.ovf_val), slots,
-                                    gm);
-                const int nsh = S.ci.w & 7;
-                T acc = Sentinel<T>::scrub(c);
-#pragma unroll
-                for (int q = 0; q < SH; ++q) {
-                    const T vq = __shfl_sync(0xffffffffu, xprev, (S.ci.w >> (3 + 5 * q)) & 31);
-                    acc = fnma(S.cv.v[1 + q], q < nsh ? vq : T(0), acc);
-                }
-                const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S.cv.v[0];
-                if (S.ci.x >= 0) __stcg(x + S.ci.x, xi);
-                if (S.ci.y >= 0) sts_flag(slots + S.ci.y, xi);
-                if (S.ci.z >= 0) stg_flag(gm + S.ci.z, xi);
-                xprev = xi;
-                // (3) step t+2's b and GLOB loads (its records have landed)
-                if (j + 2 < UB) issue_far(j & 1, rbk + (size_t)(j + 2) * REC, t + 2 < n);
-                else issue_far(j & 1, rbk1 + (size_t)(j + 2 - UB) * REC, t + 2 < n);
+        // ---- prologue
+        if (l0)
+            for (int kb = 0; kb < min(nbx, DP); ++kb) {
+                l2pf_if(gctl + (size_t)kb * UB * kCtlBytes, UB * kCtlBytes, true);
+                l2pf_if(gcoef + (size_t)kb * UB * CB, UB * CB, true);
             }
-            rslot = rslot1;
-            return true;
-        };
+        for (int kb = -DC; kb < 0; ++kb) issue(kb);     // control blocks 0..DC-1, coefficient blocks 0..DF-1
+        for (int kb = 0; kb <= (PB + UB) / UB; ++kb) wait_ctl(kb);
+        wait_coef(0);
+        __syncwarp();
+        for (int t = 0; t < PB; ++t) {
+            const int r = ctl_at(t).w;
+            prefetch_l2_if(elem(b, r), r >= 0);
+        }
 #pragma unroll 1
-        for (int k = 0; k < nblk; ++k)
-            if (!do_block(k)) break;
-        if (trc != nullptr && lane == 0) {
-            trc[g_trace_cap - 1] = wd_now();
-            for (int i = 0; i < 8; ++i) trc[g_trace_cap - 16 + i] = (unsigned long long)dbg[i];
+        for (int j = 0; j < DG; ++j) far_load(j, ctl_at(j));
+        Stage<T> S0, S1;
+        load_stage(0, S0);
+        load_stage(1, S1);
+        E3<T> E0;
+        load_ext(S0, E0);
+        cp_async_wait<DG - 1>();
+        T b0 = bland[lane];
+        int4 nx = ctl_at(DG);                   // control entry of the next far step
+        int npr = ctl_at(PB).w;                 // row of the next L2-prefetch step
+        T xprev = T(0);
+
+        // ---- main loop: UNR steps per iteration.  A step is one basic block:
+        // the chain runs speculatively on this step's EXT values while the next
+        // steps' loads are issued; the readiness check (and any ring wait)
+        // comes last, and its rare slow path redoes the chain.
+#pragma unroll 1
+        for (int t0 = 0; t0 < n; t0 += UNR) {
+#pragma unroll
+            for (int j = 0; j < UNR; ++j) {
+                const int t = t0 + j;
+                bool okc = true, okf = true;
+                if (j % UB == 0) {          // block start: refill the rings, test the next blocks
+                    const int kb = t / UB;
+                    if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();
+                    issue(kb);                           // ring slots of block kb-1 (read >= 3 steps ago)
+                    okc = try_ctl(kb + (PB + UB) / UB);  // read from the next step on
+                    okf = try_coef(kb + 1);
+                }
+                // ---- the chain on this step's values
+                const T h0 = __shfl_sync(0xffffffffu, xprev, S0.c.x);
+                const T h1 = __shfl_sync(0xffffffffu, xprev, S0.c.y);
+                const T h2 = __shfl_sync(0xffffffffu, xprev, S0.c.z);
+                T acc = b0;
+                acc = fnma(S0.f.a0, code_shfl(S0.c.x) ? h0 : E0.e0, acc);
+                acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);
+                acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
+                // ---- loads of later steps (independent of the chain)
+                far_load(t + DG, nx);
+                prefetch_l2_if(elem(b, npr), npr >= 0);
+                cp_async_wait<DG - 1>();
+                const T b1 = bland[((t + 1) & (DG - 1)) * 32 + lane];
+                E3<T> E1;
+                load_ext(S1, E1);
+                const int4 nx1 = ctl_at(t + 1 + DG);
+                const int npr1 = ctl_at(t + 1 + PB).w;
+                Stage<T> S2;
+                load_stage(t + 2, S2);
+                // ---- readiness (value-as-flag; non-EXT terms hold 0) and ring waits
+                const unsigned sh = sent_hi<T>();
+                const bool pend = (hi_word(E0.e0) == sh) | (hi_word(E0.e1) == sh) | (hi_word(E0.e2) == sh);
+                if (__any_sync(0xffffffffu, pend || !okc || !okf)) {
+                    if (!okc) wait_ctl(t / UB + (PB + UB) / UB);
+                    if (!okf) wait_coef(t / UB + 1);
+                    if (__any_sync(0xffffffffu, pend)) {
+                        E0 = repoll<T, GL>(E0, S0.c.x, S0.c.y, S0.c.z, slots, gm, status, tmo, tag);
+                        acc = b0;
+                        acc = fnma(S0.f.a0, code_shfl(S0.c.x) ? h0 : E0.e0, acc);
+                        acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);
+                        acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
+                    }
+                }
+                if (OVF) {
+                    const bool ovf = S0.c.x >= kOvfBase && code_kind(S0.c.x) == kKNone;
+                    if (__any_sync(0xffffffffu, ovf))
+                        acc = ovf_terms<T>(acc, ovf ? S0.c.x - kOvfBase : -1, xprev, a.ovf_code,
+                                           static_cast<const T *>(a.ovf_val), slots, gm, status, tmo, tag);
+                }
+                const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S0.f.invd;   // a product is never the sentinel
+                sts_flag_if(slots + S0.pub.x, xi, S0.pub.x >= 0);
+                stg_flag_if(elem(gm, S0.pub.y), xi, S0.pub.y >= 0);
+                stx_if(elem(x, S0.c.w), xi, S0.c.w >= 0);
+                xprev = xi;
+                S0 = S1;
+                S1 = S2;
+                E0 = E1;
+                b0 = b1;
+                nx = nx1;
+                npr = npr1;
+            }
         }
+        cp_async_wait<0>();
+        if (trc != nullptr && l0) trc[a.trace_cap - 1] = gtimer();
+    }
     }
 
     __syncthreads();
@@ -1141,30 +969,15 @@ __global__ void __launch_bounds__(128, 1) k_block1(const BlockArgs a) {
     }
 }
 
-template <typename T, bool UNIT>
-void *pick_kernel_lean(int W, int &we) {
-    if (W <= 3) { we = 2; return (void *)k_block1<T, UNIT, 2>; }
-    we = 4;
-    return (void *)k_block1<T, UNIT, 4>;
+template <typename T>
+void *pick_kernel(int diag, bool ovf, bool gl) {
+    if (diag == SPTRSV_UNIT) {
+        if (gl) return ovf ? (void *)k_block<T, true, true, true> : (void *)k_block<T, true, false, true>;
+        return ovf ? (void *)k_block<T, true, true, false> : (void *)k_block<T, true, false, false>;
+    }
+    if (gl) return ovf ? (void *)k_block<T, false, true, true> : (void *)k_block<T, false, false, true>;
+    return ovf ? (void *)k_block<T, false, true, false> : (void *)k_block<T, false, false, false>;
 }
-
-// per-tile shared memory of k_block (must match TILE there)
-size_t block_tile_bytes(int REC, int es, int ub) {
-    return ((size_t)kNBB * ub * REC + (size_t)kRRB * ub * 128 + (size_t)kNBB * ub * 32 * es +
-            (size_t)kBR * ub * 32 * es + 8 * (kNBB + kRRB) + 127) / 128 * 128;
-}
-
-// EXT entries per record row: enough for the detected-grid plans (7-point:
-// <= 2 EXT terms; 27-point: <= 13); more -> the overflow list
-template <typename T, bool UNIT>
-void *pick_kernel(int W, int &we) {
-    if (W <= 3) { we = 2; return (void *)k_block<T, UNIT, 2>; }
-    if (W <= 4) { we = 4; return (void *)k_block<T, UNIT, 4>; }
-    if (W <= 8) { we = 8; return (void *)k_block<T, UNIT, 8>; }
-    we = 13;
-    return (void *)k_block<T, UNIT, 13>;
-}
-bool g_host_trace = false;
 
 // Structured-grid detection: candidates (nx, nx*ny) from the dependency
 // offsets of an interior row, each verified on every dependency on the GPU.
@@ -1187,9 +1000,9 @@ sptrsv_status_t detect_grid(sptrsv_handle_t h, const int32_t *tri_ptr, const int
     for (int c : cols) offs.push_back(std::abs((int64_t)mid - c));
     std::sort(offs.begin(), offs.end());
     std::vector<std::pair<int, int>> cand3, cand2;
-    for (int64_t a : offs)
+    for (int64_t av : offs)
         for (int da = -1; da <= 1; ++da) {
-            const int64_t nx = a + da;
+            const int64_t nx = av + da;
             if (nx < 2 || nx >= n) continue;
             if (n % nx == 0 && n / nx >= 2) cand2.emplace_back((int)nx, 1);
             for (int64_t c : offs)
@@ -1245,9 +1058,12 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     } guard{tmp};
     sptrsv_status_t st = SPTRSV_SUCCESS;
     const size_t es = h->esize;
+    const bool f64 = h->dtype == SPTRSV_F64;
     int max_smem = 0;
     SPTRSV_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     const int eg = (n + 255) / 256;
+    const int CB = f64 ? Coef<double>::BYTES : Coef<float>::BYTES;
+    const size_t wsb = f64 ? warp_smem_bytes<double>() : warp_smem_bytes<float>();
 
     // ---- 1. natural-order CSR of the triangle
     int32_t *tri_ptr = nullptr, *tri_col = nullptr;
@@ -1264,7 +1080,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         if ((st = exclusive_scan_i32(dpx, tri_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     }
     const int cgrid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
-    if (h->dtype == SPTRSV_F64)
+    if (f64)
         k_tri_fill<double><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
                                                  (const double *)h->d_eval, tri_ptr, tri_col, (double *)tri_val);
     else
@@ -1272,37 +1088,14 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
                                                 (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
     SPTRSV_CUDA(cudaGetLastError());
 
-    // kernel instance (EXT entries per record row) and shared-memory budget
-    int WE = 0;
-    const int W = std::max(1, h->info.max_row_deps);
-    void *kn = nullptr;
-    if (h->dtype == SPTRSV_F64)
-        kn = h->diag == SPTRSV_UNIT ? pick_kernel<double, true>(W, WE) : pick_kernel<double, false>(W, WE);
-    else
-        kn = h->diag == SPTRSV_UNIT ? pick_kernel<float, true>(W, WE) : pick_kernel<float, false>(W, WE);
-    // lean kernel (one warp per tile, k_block1) when SPTRSV_BLOCK_LEAN=1 (opt-in:
-    // cfg2 0.327 ms vs 0.271 ms for the helper design, profiles/lean_block_r1f.md);
-    // rows with more than 4 EXT terms use the overflow lists
-    const bool lean = env_int("SPTRSV_BLOCK_LEAN", 0) != 0;
-    if (lean) {
-        if (h->dtype == SPTRSV_F64)
-            kn = h->diag == SPTRSV_UNIT ? pick_kernel_lean<double, true>(W, WE) : pick_kernel_lean<double, false>(W, WE);
-        else
-            kn = h->diag == SPTRSV_UNIT ? pick_kernel_lean<float, true>(W, WE) : pick_kernel_lean<float, false>(W, WE);
-    }
-    const int REC = rec_bytes(kSH, WE, (int)es);
     const size_t budget = (size_t)max_smem - 1024;          // static smem + slack
-    // per CTA (nt tiles): the tiles' rings; the rest holds shared slots
-    auto ring_bytes = [&](int nt) {
-        return (size_t)nt * (lean ? lean_tile_bytes_c(REC, (int)es) : block_tile_bytes(REC, (int)es, ub_of(WE)));
-    };
 
     // ---- 2. partition rows over U = K x wpc warps of K co-resident CTAs
     int32_t *unit = nullptr;
     if ((st = h->arena.alloc_n(&unit, n)) != SPTRSV_SUCCESS) return st;
     B.d_unit = unit;
     int gnx = 0, gny = 0;
-    if (n >= 64 && !env_int("SPTRSV_BLOCK_NO_GRID", 0)) {
+    if (n >= 64) {
         if ((st = detect_grid(h, tri_ptr, tri_col, tmp, s, gnx, gny)) != SPTRSV_SUCCESS) return st;
     }
     int K = 1, wpc = 4;
@@ -1310,18 +1103,12 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     if (gnx > 0) {
         // warp tile tw x th columns (<= 32: one step per level), CTA = wx x wy
         // tiles; the fewest warps per CTA that fit all CTAs on the SMs
-        int tw = std::min(env_int("SPTRSV_BLOCK_TW", gny == 1 ? 32 : 8), gnx);
+        int tw = std::min(gny == 1 ? 32 : 8, gnx);
         int th = std::max(1, std::min(32 / std::max(tw, 1), gny));
-        const int ewx = env_int("SPTRSV_BLOCK_WX", 0), ewy = env_int("SPTRSV_BLOCK_WY", 0);
         static const int shapes[][2] = {{1, 1}, {2, 1}, {1, 2}, {2, 2}};
         int wx = 0, wy = 0;
         for (int grow = 0; grow < 8 && wx == 0; ++grow) {
             const int ntx = (gnx + tw - 1) / tw, nty = (gny + th - 1) / th;
-            if (ewx > 0 && ewy > 0) {
-                wx = ewx;
-                wy = ewy;
-                break;
-            }
             for (auto &sh : shapes) {
                 if (sh[0] > ntx && sh[0] > 1) continue;
                 if (sh[1] > nty && sh[1] > 1) continue;
@@ -1343,7 +1130,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             K = cxn * cyn;
             wpc = wx * wy;
             if (K > h->num_sms) return SPTRSV_ERR_NOT_SUPPORTED;
-            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, tw, th, wx, wy, cxn, unit);
+            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, tw, th, wx, wy, cxn, K, h->uplo == SPTRSV_UPPER, unit);
             B.grid_nx = gnx;
             B.grid_ny = gny;
             B.tile_w = tw;
@@ -1353,11 +1140,9 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         }
     }
     if (gnx == 0) {
-        int Kn = env_int("SPTRSV_BLOCK_K", 0);
-        if (Kn <= 0) Kn = (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, n / 8192));
-        K = std::min(Kn, h->num_sms);
+        K = (int)std::max<int64_t>(1, std::min<int64_t>(h->num_sms, n / 8192));
         wpc = 4;
-        while (wpc > 1 && ring_bytes(wpc) + 2048 * es > budget) wpc /= 2;
+        while (wpc > 1 && (size_t)wpc * wsb + 2048 * es > budget) wpc /= 2;
         k_part_natural<<<eg, 256, 0, s>>>(n, K * wpc, h->uplo, unit);
     }
     SPTRSV_CUDA(cudaGetLastError());
@@ -1402,267 +1187,172 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     if ((st = tmp.alloc_n(&step_unit, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&step_of, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&cta_p0, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
+    int32_t *unit_step0 = nullptr, *pcnt = nullptr, *pmap = nullptr;
+    if ((st = tmp.alloc_n(&unit_step0, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&pcnt, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&pmap, (size_t)nsteps + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc_n(&B.d_unit_step0, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
     k_steps<<<gg, 256, 0, s>>>(gp0, sub0, ngroups, bperm, unit, steps, step_unit);
-    k_unit_step0<<<(nsteps + 255) / 256, 256, 0, s>>>(step_unit, nsteps, U, B.d_unit_step0);
+    k_unit_step0<<<(nsteps + 255) / 256, 256, 0, s>>>(step_unit, nsteps, U, unit_step0);
     k_pos_step<<<eg, 256, 0, s>>>(head, gid, gp0, sub0, n, step_of);
-    k_cta_p0<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, wpc, nsteps, n, B.d_unit_step0, steps, cta_p0);
+    k_cta_p0<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, wpc, nsteps, n, unit_step0, steps, cta_p0);
+    // every warp's steps padded to a multiple of UNR (empty steps): padded starts, step -> padded step
+    k_pad_count<<<(U + 1 + 255) / 256, 256, 0, s>>>(U, unit_step0, pcnt);
+    if ((st = exclusive_scan_i32(pcnt, B.d_unit_step0, (int64_t)U + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    k_pad_map<<<(nsteps + 255) / 256, 256, 0, s>>>(nsteps, step_unit, unit_step0, B.d_unit_step0, pmap);
+    const int32_t npad = i32_at(B.d_unit_step0, U, s, st);
+    if (st != SPTRSV_SUCCESS) return st;
+    B.npad = npad;
     SPTRSV_CUDA(cudaGetLastError());
 
-    // ---- 4. shared-memory budget, dependency classes
-    auto fixed_bytes = [&]() { return ring_bytes(wpc); };
-    if (fixed_bytes() > budget) return SPTRSV_ERR_NOT_SUPPORTED;
-    const int cap = (int)((budget - fixed_bytes()) / es);
-
+    // ---- 4. shared-memory budget, dependency classes, inbound items
+    const size_t fixed = (size_t)wpc * wsb;
+    if (fixed > budget) return SPTRSV_ERR_NOT_SUPPORTED;
+    const int cap = (int)((budget - fixed) / es);
     unsigned char *noslot = nullptr;
     int32_t *need = nullptr, *bits = nullptr, *slot_scan = nullptr, *g_scan = nullptr, *ccnt = nullptr;
-    int32_t *ecnt = nullptr;
-    if ((st = tmp.alloc_n(&ecnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    int32_t *icnt = nullptr, *iptr = nullptr;
     if ((st = tmp.alloc_n(&noslot, (size_t)K)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&need, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&bits, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&slot_scan, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&g_scan, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&ccnt, (size_t)K)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&icnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&iptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(noslot, 0, (size_t)K, s));
-    std::vector<int32_t> hcnt(K);
-    std::vector<unsigned char> hns(K, 0);
+    // intra-CTA slots (need bit 0), mailboxes (bit 1), cross dependencies per position
+    SPTRSV_CUDA(cudaMemsetAsync(need, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+    k_need<<<eg, 256, 0, s>>>(n, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need, icnt);
+    k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
+    if ((st = exclusive_scan_i32(bits, slot_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    if ((st = exclusive_scan_i32(icnt, iptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, iptr, ccnt);
+    SPTRSV_CUDA(cudaGetLastError());
+    std::vector<int32_t> hcnt(2 * (size_t)K);
+    SPTRSV_CUDA(cudaMemcpyAsync(hcnt.data(), ccnt, sizeof(int32_t) * K, cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    // every CTA's intra + inbound slots fit: fetcher mode; else GLOB terms
+    // (GL instance), and CTAs whose intra slots do not fit use mailboxes too
+    bool gl = false;
     int max_slots = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        SPTRSV_CUDA(cudaMemsetAsync(need, 0, sizeof(int32_t) * ((size_t)n + 1), s));
-        k_need<<<eg, 256, 0, s>>>(n, kSH, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need, ecnt);
-        k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
-        if ((st = exclusive_scan_i32(bits, slot_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-        k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, ccnt);
-        SPTRSV_CUDA(cudaGetLastError());
+    for (int c = 0; c < K; ++c) {
+        gl |= hcnt[c] > cap;        // hcnt: intra + inbound
+        max_slots = std::max(max_slots, hcnt[c]);
+    }
+    int32_t nitems = 0;
+    if (gl) {
+        k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, nullptr, ccnt);   // intra only
         SPTRSV_CUDA(cudaMemcpyAsync(hcnt.data(), ccnt, sizeof(int32_t) * K, cudaMemcpyDeviceToHost, s));
         SPTRSV_CUDA(cudaStreamSynchronize(s));
+        std::vector<unsigned char> hns(K, 0);
         bool over = false;
         max_slots = 0;
         for (int c = 0; c < K; ++c) {
-            if (hcnt[c] > cap) {
-                hns[c] = 1;
-                over = true;
-            } else {
-                max_slots = std::max(max_slots, hcnt[c]);
-            }
+            if (hcnt[c] > cap) hns[c] = 1, over = true;
+            else max_slots = std::max(max_slots, hcnt[c]);
         }
-        if (!over) break;
-        if (pass == 1) return SPTRSV_ERR_NOT_SUPPORTED;
-        SPTRSV_CUDA(cudaMemcpyAsync(noslot, hns.data(), (size_t)K, cudaMemcpyHostToDevice, s));
+        if (over) {
+            SPTRSV_CUDA(cudaMemcpyAsync(noslot, hns.data(), (size_t)K, cudaMemcpyHostToDevice, s));
+            SPTRSV_CUDA(cudaMemsetAsync(need, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+            k_need<<<eg, 256, 0, s>>>(n, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need, icnt);
+            k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
+            if ((st = exclusive_scan_i32(bits, slot_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+        }
+    } else {
+        nitems = i32_at(iptr, n, s, st);
+        if (st != SPTRSV_SUCCESS) return st;
     }
+    B.gl = gl;
     k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 1, bits);
     if ((st = exclusive_scan_i32(bits, g_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     const int32_t G = i32_at(g_scan, n, s, st);
     if (st != SPTRSV_SUCCESS) return st;
-    B.G = G;
+    B.G = (G + 3) / 4 * 4;             // mailbox array stride (16-byte aligned arrays)
     B.nslots = max_slots;
-    // per-CTA mailbox ranges: [g_scan[cta_p0[c]], g_scan[cta_p0[c+1]])
     if ((st = h->arena.alloc_n(&B.d_cta_g0, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
-    {
-        std::vector<int32_t> hp0(K + 1), hg0(K + 1);
-        SPTRSV_CUDA(cudaMemcpyAsync(hp0.data(), cta_p0, sizeof(int32_t) * (K + 1), cudaMemcpyDeviceToHost, s));
-        SPTRSV_CUDA(cudaStreamSynchronize(s));
-        for (int c = 0; c <= K; ++c) {
-            hg0[c] = i32_at(g_scan, hp0[c], s, st);
-            if (st != SPTRSV_SUCCESS) return st;
-        }
-        SPTRSV_CUDA(cudaMemcpyAsync(B.d_cta_g0, hg0.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    k_cta_g0<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, cta_p0, g_scan, B.d_cta_g0);
+    // inbound items {mailbox, slot} sorted by (CTA, level); rank of every item
+    int32_t *irank = nullptr;
+    if ((st = h->arena.alloc_n(&B.d_fptr, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_fitems, (size_t)std::max(nitems, 1))) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&irank, (size_t)std::max(nitems, 1))) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(B.d_fptr, 0, sizeof(int32_t) * ((size_t)K + 1), s));
+    if (nitems > 0) {
+        uint32_t *ikey = nullptr, *iskey = nullptr;
+        int32_t *imb = nullptr, *iperm = nullptr;
+        if ((st = tmp.alloc_n(&ikey, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&iskey, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&imb, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&iperm, nitems)) != SPTRSV_SUCCESS) return st;
+        k_items<<<eg, 256, 0, s>>>(n, nlev, wpc, bperm, tri_ptr, tri_col, unit, pos, step_of, h->d_lev, g_scan,
+                                   iptr, ikey, imb);
+        if ((st = radix_sort_pairs(ikey, nullptr, iskey, iperm, nitems, (uint32_t)((uint64_t)K * nlev - 1), tmp, s)) !=
+            SPTRSV_SUCCESS)
+            return st;
+        k_cta_iptr<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, cta_p0, iptr, B.d_fptr);
+        k_item_place<<<(nitems + 255) / 256, 256, 0, s>>>(nitems, K, nlev, iskey, iperm, imb, slot_scan, cta_p0,
+                                                           B.d_fptr, B.d_fitems, irank);
+        SPTRSV_CUDA(cudaGetLastError());
     }
+    B.nitems = nitems;
 
     // ---- 5. overflow lists and records
     int32_t *ocnt = nullptr, *ovf_ptr = nullptr;
     if ((st = tmp.alloc_n(&ocnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&ovf_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, WE, ecnt, ocnt);
+    k_ovf_count<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, bperm, h->d_dp, ocnt);
     if ((st = exclusive_scan_i32(ocnt, ovf_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     const int32_t novf = i32_at(ovf_ptr, n, s, st);
     if (st != SPTRSV_SUCCESS) return st;
     B.novf = novf;
-    // + 4 padding steps: a warp's last block of records / row ids is copied whole
-    if ((st = h->arena.alloc(&B.d_recs, (size_t)((int64_t)nsteps + 4) * REC)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_rows, (size_t)((int64_t)nsteps + 4) * 32)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync((unsigned char *)B.d_recs + (size_t)nsteps * REC, 0xFF, (size_t)4 * REC, s));
-    SPTRSV_CUDA(cudaMemsetAsync(B.d_rows + (size_t)nsteps * 32, 0xFF, (size_t)4 * 128, s));
+    // + kPadSteps: a warp's last block of records / row ids is copied whole
+    const size_t nrec = (size_t)npad + kPadSteps;
+    if ((st = h->arena.alloc(&B.d_ctl, nrec * kCtlBytes)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc(&B.d_coef, nrec * CB)) != SPTRSV_SUCCESS) return st;
+    {
+        const int fgp = (int)std::max<int64_t>(1, ((int64_t)nrec * 32 + 255) / 256);
+        if (f64) k_pad_fill<double><<<fgp, 256, 0, s>>>((int64_t)nrec, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef);
+        else k_pad_fill<float><<<fgp, 256, 0, s>>>((int64_t)nrec, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef);
+    }
     if ((st = h->arena.alloc_n(&B.d_ovf_code, (size_t)std::max(novf, 1))) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc(&B.d_ovf_val, (size_t)std::max(novf, 1) * es)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc(&B.d_gmb, (size_t)2 * std::max(G, 1) * es)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_ctr, 2)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(B.d_ctr, 0, 2 * sizeof(unsigned), s));
+    if ((st = h->arena.alloc(&B.d_gmb, (size_t)2 * std::max(B.G, 4) * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_ctr, 4)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(B.d_ctr, 0, 4 * sizeof(unsigned), s));
     const int pg = (int)std::max<int64_t>(1, ((int64_t)nsteps * 32 + 255) / 256);
-    const int fg = std::max(1, std::min((int)((2 * (int64_t)std::max(G, 1) + 255) / 256), h->num_sms * 8));
-    if (h->dtype == SPTRSV_F64) {
-        k_rec_fill<double><<<pg, 256, 0, s>>>(nsteps, kSH, WE, wpc, steps, bperm, pos, step_of, unit, tri_ptr,
-                                              tri_col, (const double *)tri_val, (const double *)h->d_invd_row,
-                                              h->diag == SPTRSV_UNIT, noslot, need, ecnt, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
-                                              B.d_rows, B.d_ovf_code, (double *)B.d_ovf_val);
-        k_fill_sentinel<double><<<fg, 256, 0, s>>>((double *)B.d_gmb, 2 * (int64_t)std::max(G, 1));
+    const int fg = std::max(1, std::min((int)((2 * (int64_t)std::max(B.G, 4) + 255) / 256), h->num_sms * 8));
+    if (f64) {
+        k_rec_fill<double><<<pg, 256, 0, s>>>(nsteps, wpc, steps, pmap, bperm, pos, step_of, unit, tri_ptr, tri_col,
+                                              (const double *)tri_val, (const double *)h->d_invd_row,
+                                              h->diag == SPTRSV_UNIT, noslot, need, slot_scan, g_scan, cta_p0,
+                                              ovf_ptr, iptr, irank, (int)gl, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
+                                              (double *)B.d_ovf_val);
+        k_fill_sentinel<double><<<fg, 256, 0, s>>>((double *)B.d_gmb, 2 * (int64_t)std::max(B.G, 4));
     } else {
-        k_rec_fill<float><<<pg, 256, 0, s>>>(nsteps, kSH, WE, wpc, steps, bperm, pos, step_of, unit, tri_ptr,
-                                             tri_col, (const float *)tri_val, (const float *)h->d_invd_row,
-                                             h->diag == SPTRSV_UNIT, noslot, need, ecnt, slot_scan, g_scan, cta_p0, ovf_ptr, (unsigned char *)B.d_recs,
-                                             B.d_rows, B.d_ovf_code, (float *)B.d_ovf_val);
-        k_fill_sentinel<float><<<fg, 256, 0, s>>>((float *)B.d_gmb, 2 * (int64_t)std::max(G, 1));
+        k_rec_fill<float><<<pg, 256, 0, s>>>(nsteps, wpc, steps, pmap, bperm, pos, step_of, unit, tri_ptr, tri_col,
+                                             (const float *)tri_val, (const float *)h->d_invd_row,
+                                             h->diag == SPTRSV_UNIT, noslot, need, slot_scan, g_scan, cta_p0,
+                                             ovf_ptr, iptr, irank, (int)gl, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
+                                             (float *)B.d_ovf_val);
+        k_fill_sentinel<float><<<fg, 256, 0, s>>>((float *)B.d_gmb, 2 * (int64_t)std::max(B.G, 4));
     }
     SPTRSV_CUDA(cudaGetLastError());
 
-    // ---- launch configuration: K co-resident CTAs of wpc tiles (2 warps each)
-    const size_t smem = fixed_bytes() + (size_t)max_slots * es;
+    // ---- launch configuration: K co-resident CTAs of wpc warps
+    void *kn = f64 ? pick_kernel<double>(h->diag, novf > 0, gl) : pick_kernel<float>(h->diag, novf > 0, gl);
+    const size_t smem = fixed + (size_t)max_slots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    const int tpw = lean ? 32 : 96;          // threads per tile
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, tpw * wpc, smem));
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 32 * (wpc + 1), smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = tpw * wpc;
-    B.lean = lean;
-    B.nst = lean ? kLNBB * kLUB : kNBB * ub_of(WE);
-    B.bb = lean ? 2 : kR2B * ub_of(WE);
-    B.d = lean ? kLDB * kLUB : kDB * ub_of(WE);
-    B.W = WE;
-    B.rec_bytes = REC;
-    B.nent = (int64_t)nsteps * REC;
+    B.threads = 32 * (wpc + 1);          // wpc compute warps + the fetcher
+    B.rec_bytes = kCtlBytes + CB;
+    B.nent = (int64_t)npad * (kCtlBytes + CB);
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     B.built = true;
-    return SPTRSV_SUCCESS;
-}
-
-// ---------------------------------------------------------------- CTA-tile multi-RHS plan
-// Positions sorted by (CTA, level, row) with the BLOCK partition's CTAs; a
-// per-position CSR (same shape as the level-ordered multi-RHS CSR, so the
-// row kernels are shared); per (CTA, level) position ranges; per CTA the list
-// of CTAs that produce its dependencies.  k_tile_mrhs (solve.cu) walks each
-// CTA's levels with __syncthreads between them and waits only for its
-// producer CTAs' level counters: no grid-wide barrier.
-__global__ void k_tm_keys(int n, int nlev, int wpc, const int32_t *unit, const int32_t *lev, uint32_t *keys,
-                          int32_t *cnt) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = (uint32_t)(unit[i] / wpc) * (uint32_t)nlev + (uint32_t)lev[i];
-    keys[i] = k;
-    atomicAdd(&cnt[k], 1);
-}
-
-template <typename T>
-__global__ void k_tm_rows(int n, const int32_t *perm, const int32_t *dp, const T *invd_row, int unit_diag,
-                          T *invd, int32_t *deg) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < n) {
-        const int i = perm[p];
-        invd[p] = unit_diag ? T(1) : invd_row[i];
-        deg[p] = dp[i];
-    }
-    if (p == n) deg[p] = 0;
-}
-
-template <typename T>
-__global__ void k_tm_fill(int n, int K, int wpc, const int32_t *perm, const int32_t *tri_ptr, const int32_t *tri_col,
-                          const T *tri_val, const int32_t *unit, const int32_t *ptr, int32_t *col, T *val,
-                          unsigned char *depm) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const int i = perm[p];
-    const int ci = unit[i] / wpc;
-    int o = ptr[p];
-    for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k, ++o) {
-        const int j = tri_col[k];
-        col[o] = j;
-        val[o] = tri_val[k];
-        const int cj = unit[j] / wpc;
-        if (cj != ci) depm[(size_t)ci * K + cj] = 1;
-    }
-}
-
-sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s) {
-    BlockPlan &B = h->block;
-    if (!B.built || B.grid_nx == 0) return SPTRSV_ERR_NOT_SUPPORTED;
-    const int n = h->n, nlev = h->info.nlev, K = B.nblocks, wpc = B.wpc;
-    const size_t es = h->esize;
-    if ((uint64_t)K * (uint64_t)nlev >= (1ull << 31)) return SPTRSV_ERR_NOT_SUPPORTED;
-    DevArena tmp;
-    struct Guard {
-        DevArena &a;
-        ~Guard() { a.release_all(); }
-    } guard{tmp};
-    sptrsv_status_t st;
-    const int eg = (n + 256) / 256;
-    // natural-order CSR of the triangle (as in block_build)
-    int32_t *tri_ptr = nullptr, *tri_col = nullptr, *dpx = nullptr;
-    void *tri_val = nullptr;
-    const int64_t nnz = std::max<int64_t>(h->info.nnz_used, 1);
-    if ((st = tmp.alloc_n(&tri_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&tri_col, (size_t)nnz)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc(&tri_val, (size_t)nnz * es)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&dpx, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemcpyAsync(dpx, h->d_dp, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-    SPTRSV_CUDA(cudaMemsetAsync(dpx + n, 0, sizeof(int32_t), s));
-    if ((st = exclusive_scan_i32(dpx, tri_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    const int cgrid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
-    if (h->dtype == SPTRSV_F64)
-        k_tri_fill<double><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
-                                                 (const double *)h->d_eval, tri_ptr, tri_col, (double *)tri_val);
-    else
-        k_tri_fill<float><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
-                                                (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
-    // order by (CTA, level, row); (CTA, level) offsets
-    const int64_t KL = (int64_t)K * nlev;
-    uint32_t *keys = nullptr, *skeys = nullptr;
-    int32_t *cnt = nullptr, *deg = nullptr;
-    unsigned char *depm = nullptr;
-    if ((st = tmp.alloc_n(&keys, n)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&skeys, n)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&cnt, (size_t)KL + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&deg, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&depm, (size_t)K * K)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_perm, n)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc(&B.d_tm_invd, (size_t)n * es)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_col, (size_t)nnz)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc(&B.d_tm_val, (size_t)nnz * es)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_off, (size_t)KL + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_done, (size_t)K)) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)KL + 1), s));
-    SPTRSV_CUDA(cudaMemsetAsync(depm, 0, (size_t)K * K, s));
-    SPTRSV_CUDA(cudaMemsetAsync(B.d_tm_done, 0, sizeof(unsigned long long) * K, s));
-    k_tm_keys<<<eg, 256, 0, s>>>(n, nlev, wpc, B.d_unit, h->d_lev, keys, cnt);
-    if ((st = radix_sort_pairs(keys, nullptr, skeys, B.d_tm_perm, n, (uint32_t)(KL - 1), tmp, s)) != SPTRSV_SUCCESS)
-        return st;
-    if ((st = exclusive_scan_i32(cnt, B.d_tm_off, (int64_t)KL + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    if (h->dtype == SPTRSV_F64)
-        k_tm_rows<double><<<eg, 256, 0, s>>>(n, B.d_tm_perm, h->d_dp, (const double *)h->d_invd_row,
-                                             h->diag == SPTRSV_UNIT, (double *)B.d_tm_invd, deg);
-    else
-        k_tm_rows<float><<<eg, 256, 0, s>>>(n, B.d_tm_perm, h->d_dp, (const float *)h->d_invd_row,
-                                            h->diag == SPTRSV_UNIT, (float *)B.d_tm_invd, deg);
-    if ((st = exclusive_scan_i32(deg, B.d_tm_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    if (h->dtype == SPTRSV_F64)
-        k_tm_fill<double><<<eg, 256, 0, s>>>(n, K, wpc, B.d_tm_perm, tri_ptr, tri_col, (const double *)tri_val,
-                                             B.d_unit, B.d_tm_ptr, B.d_tm_col, (double *)B.d_tm_val, depm);
-    else
-        k_tm_fill<float><<<eg, 256, 0, s>>>(n, K, wpc, B.d_tm_perm, tri_ptr, tri_col, (const float *)tri_val,
-                                            B.d_unit, B.d_tm_ptr, B.d_tm_col, (float *)B.d_tm_val, depm);
-    SPTRSV_CUDA(cudaGetLastError());
-    // producer lists
-    std::vector<unsigned char> hdep((size_t)K * K);
-    SPTRSV_CUDA(cudaMemcpyAsync(hdep.data(), depm, (size_t)K * K, cudaMemcpyDeviceToHost, s));
-    SPTRSV_CUDA(cudaStreamSynchronize(s));
-    std::vector<int32_t> dptr(K + 1, 0), dl;
-    for (int c = 0; c < K; ++c) {
-        for (int p = 0; p < K; ++p)
-            if (hdep[(size_t)c * K + p]) dl.push_back(p);
-        dptr[c + 1] = (int32_t)dl.size();
-    }
-    if (dl.empty()) dl.push_back(0);
-    if ((st = h->arena.alloc_n(&B.d_tm_dptr, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_tm_dl, dl.size())) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemcpyAsync(B.d_tm_dptr, dptr.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
-    SPTRSV_CUDA(cudaMemcpyAsync(B.d_tm_dl, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice, s));
-    SPTRSV_CUDA(cudaStreamSynchronize(s));
-    B.tm_K = K;
-    B.tm_base = 0;
-    B.tm_built = true;
-    h->info.device_bytes = h->arena.bytes;
     return SPTRSV_SUCCESS;
 }
 
@@ -1671,43 +1361,37 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     if (!B.built) return SPTRSV_ERR_NOT_SUPPORTED;
     BlockArgs a;
     a.unit_step0 = B.d_unit_step0;
-    a.recs = (const unsigned char *)B.d_recs;
-    a.rows = B.d_rows;
+    a.ctl = (const unsigned char *)B.d_ctl;
+    a.coef = (const unsigned char *)B.d_coef;
     a.cta_g0 = B.d_cta_g0;
+    a.fitems = B.d_fitems;
+    a.fptr = B.d_fptr;
     a.ovf_code = B.d_ovf_code;
     a.ovf_val = B.d_ovf_val;
     a.gmb = B.d_gmb;
     a.ctr = B.d_ctr;
+    a.status = B.d_ctr + 2;
+    a.trace = static_cast<unsigned long long *>(B.trace);
+    a.trace_cap = B.trace_cap;
     a.b = b;
     a.x = x;
     a.G = B.G;
     a.nslots = B.nslots;
+    a.timeout_ns = h->timeout_ns;
     void *args[] = {(void *)&a};
     SPTRSV_CUDA(cudaLaunchCooperativeKernel(B.kernel, B.nblocks, B.threads, args, B.smem, s));
+    h->last_block_solve = true;
     return SPTRSV_SUCCESS;
 }
 
+// TIMEOUT iff the last BLOCK solve on the handle gave up a wait: its status
+// word holds the solve's epoch + 1 and the epoch counter has advanced past it.
+sptrsv_status_t block_solve_status(sptrsv_handle_t h) {
+    BlockPlan &B = h->block;
+    if (!B.built || !h->last_block_solve) return SPTRSV_SUCCESS;
+    unsigned c[4] = {0, 0, 0, 0};
+    SPTRSV_CUDA(cudaMemcpy(c, B.d_ctr, sizeof(c), cudaMemcpyDeviceToHost));
+    return (c[2] != 0 && c[2] == c[0]) ? SPTRSV_ERR_TIMEOUT : SPTRSV_SUCCESS;
+}
+
 }  // namespace sptrsv
-
-// Debug hook (not part of include/sptrsv.h): install a device trace buffer of
-// (#warps) x cap uint64 timestamps for SPTRSV_ALGO_BLOCK solves (NULL disables).
-extern "C" int sptrsv_dbg_block_trace(void *dev_buf, int cap) {
-    unsigned long long *p = (unsigned long long *)dev_buf;
-    if (cudaMemcpyToSymbol(sptrsv::g_trace, &p, sizeof(p)) != cudaSuccess) return 5;
-    if (cudaMemcpyToSymbol(sptrsv::g_trace_cap, &cap, sizeof(int)) != cudaSuccess) return 5;
-    sptrsv::g_host_trace = (dev_buf != nullptr);
-    return 0;
-}
-
-extern "C" int sptrsv_dbg_block_phase(void *dev_buf) {
-    unsigned long long *p = (unsigned long long *)dev_buf;
-    return cudaMemcpyToSymbol(sptrsv::g_phase, &p, sizeof(p)) == cudaSuccess ? 0 : 5;
-}
-
-// Debug hook: returns and clears the spin-watchdog flag (1 = a wait gave up).
-extern "C" int sptrsv_dbg_watchdog(void) {
-    unsigned v = 0, z = 0;
-    cudaMemcpyFromSymbol(&v, sptrsv::g_watchdog, sizeof(v));
-    cudaMemcpyToSymbol(sptrsv::g_watchdog, &z, sizeof(z));
-    return (int)v;
-}

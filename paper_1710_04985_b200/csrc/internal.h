@@ -33,60 +33,33 @@ struct DevArena {
 // Block-schedule (SPTRSV_ALGO_BLOCK) device data; see block.cu.
 struct BlockPlan {
     bool built = false;
-    bool lean = false;        // k_block1 (one warp per tile) instead of k_block
     int32_t nblocks = 0;      // K co-resident CTAs
-    int32_t wpc = 0;          // tiles per CTA
-    int32_t nunits = 0;       // K x wpc tiles (a compute and a helper warp each)
-    int32_t W = 0;            // EXT entries per record row (kernel instance)
-    int32_t nst = 0;          // record ring per warp (steps)
-    int32_t bb = 0;           // b lookahead (steps)
-    int32_t d = 0;            // record lookahead (steps)
-    int32_t r1 = 0, rr = 0;   // row-id lookahead / ring (steps)
+    int32_t wpc = 0;          // warp tiles per CTA
+    int32_t nunits = 0;       // K x wpc tiles (one warp each)
     int32_t nsteps = 0;       // (warp, level) steps of <= 32 rows
+    int32_t npad = 0;         // steps after padding every warp to a multiple of the loop unroll
     int32_t G = 0;            // global mailboxes (values read by another CTA)
     int32_t nslots = 0;       // shared slots per CTA (values read by another warp of the CTA)
-    int32_t novf = 0, threads = 0, rec_bytes = 0;
+    int32_t novf = 0, threads = 0, rec_bytes = 0;   // rec_bytes: both streams, per step
     int32_t grid_nx = 0, grid_ny = 0, tile_w = 0, tile_h = 0;   // detected grid / warp tile (0 = natural)
     int64_t nent = 0;         // record bytes
     size_t smem = 0;
     void *kernel = nullptr;
     int32_t *d_unit_step0 = nullptr;  // [U+1] first step of every warp
-    void *d_recs = nullptr;           // step records (see block.cu)
-    int32_t *d_rows = nullptr;        // [nsteps][32] row ids (b gather addresses)
+    void *d_ctl = nullptr;            // step records: control stream (see block.cu)
+    void *d_coef = nullptr;           // step records: coefficient stream
     int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
-    int32_t *d_ovf_code = nullptr;    // overflow entries (rows with > W dependencies)
+    int2 *d_fitems = nullptr;         // inbound items {mailbox, shared slot} by (CTA, level) (fetcher warps)
+    int32_t *d_fptr = nullptr;        // [K+1] inbound item range of every CTA
+    int32_t nitems = 0;
+    bool gl = false;                  // fallback: consumers poll mailboxes themselves (slots did not fit)
+    int32_t *d_ovf_code = nullptr;    // overflow lists (rows with > 3 dependencies)
     void *d_ovf_val = nullptr;
     void *d_gmb = nullptr;            // [2][G] mailboxes (value-as-flag), roles swap per solve
-    unsigned *d_ctr = nullptr;        // [0] solve epoch, [1] finished CTAs
+    unsigned *d_ctr = nullptr;        // [0] solve epoch, [1] finished CTAs, [2] timed-out epoch + 1
     int32_t *d_unit = nullptr;        // [n] warp tile of every row (CTA = unit / wpc)
-    // CTA-tile multi-RHS plan (built on the first multi-RHS BLOCK solve; see block.cu)
-    bool tm_built = false;
-    int32_t tm_K = 0;
-    int32_t *d_tm_perm = nullptr;     // [n] position -> row, positions sorted by (CTA, level, row)
-    void *d_tm_invd = nullptr;        // [n] 1/d by position
-    int32_t *d_tm_ptr = nullptr;      // [n+1] CSR of the referenced strict triangle by position
-    int32_t *d_tm_col = nullptr;
-    void *d_tm_val = nullptr;
-    int32_t *d_tm_off = nullptr;      // [K*nlev+1] first position of (CTA, level)
-    int32_t *d_tm_dptr = nullptr;     // [K+1] producer-CTA lists
-    int32_t *d_tm_dl = nullptr;
-    unsigned long long *d_tm_done = nullptr;   // [K] levels completed (epoch based, monotone)
-    unsigned long long tm_base = 0;
-};
-
-// CTA-tile level-synchronous plan (SPTRSV_ALGO_TILE); see tile.cu.
-struct TilePlan {
-    bool built = false;
-    int32_t K = 0, threads = 0, maxr = 0;
-    size_t smem = 0;
-    void *kernel = nullptr;
-    int4 *d_clist = nullptr;          // per CTA non-empty levels {level, first position, rows, 0}
-    int32_t *d_cptr = nullptr;        // [K+1]
-    int32_t *d_cpos = nullptr;        // [K+1] first position of every CTA
-    int4 *d_ri = nullptr;             // [n] {row, code0..2}
-    void *d_rv = nullptr;             // [n][4] {1/d, v0..v2}
-    unsigned long long *d_done = nullptr;   // [K] level counters (epoch based)
-    unsigned long long base = 0;
+    void *trace = nullptr;            // debug (sptrsv_dbg_block_trace): per-warp step timestamps
+    int32_t trace_cap = 0;
 };
 
 }  // namespace sptrsv
@@ -137,15 +110,16 @@ struct sptrsv_handle_s {
     unsigned *d_ctr = nullptr;               // [0] ticket, [1] exit count (self / mrhs)
     unsigned long long *d_bar = nullptr;     // level barrier counter (monotone)
     unsigned long long bar_base = 0;
-    int32_t self_grid = 0, level_grid = 0, mrhs_grid = 0;
-    bool self_u16 = false;                   // k_self instance of self_grid (SPTRSV_WPR_U)
+    int32_t self_grid = 0, vf_grid = 0;       // resident grids (computed on first use)
     // in-place / host staging
     void *d_stage = nullptr;
     size_t stage_bytes = 0;
     void *d_scratch = nullptr;               // copy of b for in-place value-as-flag solves
     size_t scratch_bytes = 0;
     sptrsv::BlockPlan block;
-    sptrsv::TilePlan tile;
+    // spin watchdog of the BLOCK solve (sptrsv_get_solve_status)
+    unsigned long long timeout_ns = 4000000000ull;
+    bool last_block_solve = false;
 };
 
 namespace sptrsv {
@@ -154,9 +128,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
-sptrsv_status_t tile_mrhs_build(sptrsv_handle_t h, cudaStream_t s);
-sptrsv_status_t tile_build(sptrsv_handle_t h, cudaStream_t s);
-sptrsv_status_t tile_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
+sptrsv_status_t block_solve_status(sptrsv_handle_t h);
 sptrsv_status_t column_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);   // column.cu
 sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s);                            // solve.cu
 // device scans (analyze.cu)

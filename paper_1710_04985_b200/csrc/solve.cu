@@ -83,26 +83,6 @@ __device__ __forceinline__ void reload_pending(const int (&c)[N], T (&v)[N], con
     for (int u = 0; u < N; ++u)
         if (c[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + c[u]);
 }
-// Thread-per-row poll: only the LAST pending dependency in storage order (the
-// nearest row, in practice the critical one from the previous level) is
-// re-loaded, and every 4th round all pending ones.  Re-loading every pending
-// value each round made 2,400 spinning warps flood L2 with polls (cfg3, 13
-// dependencies per row: 3.2 us from ready to published, tools/self_trace.py).
-template <typename T, int N>
-__device__ __forceinline__ void reload_pending_lazy(const int (&c)[N], T (&v)[N], const T *x, unsigned it) {
-    if ((it & 3u) == 0) {
-        reload_pending<T, N>(c, v, x);
-        return;
-    }
-    int last = -1;
-#pragma unroll
-    for (int u = 0; u < N; ++u)
-        if (c[u] >= 0 && Sentinel<T>::is(v[u])) last = u;
-#pragma unroll
-    for (int u = 0; u < N; ++u)
-        if (u == last) v[u] = ld_relaxed_val(x + c[u]);
-}
-
 // ---------------------------------------------------------------- TPR row
 // One chunk of up to 32 rows, thread per row.  Entry k of lane r at
 // eptr + k*32 + r.  WAIT: dependencies are polled as VALUES (value-as-flag,
@@ -114,8 +94,7 @@ template <typename T, bool UNIT, bool WAIT>
 __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const int32_t *__restrict__ perm,
                                           const T *__restrict__ invd, const int32_t *__restrict__ ecol,
                                           const T *__restrict__ eval, const T *b, T *x,
-                                          unsigned long long *tp = nullptr, int lazy_w = kTprMax,
-                                          unsigned sleep_ns = 20) {
+                                          unsigned long long *tp = nullptr) {
     const int nr = chunk_nrows(cd.meta), width = chunk_width(cd.meta);
     const bool act = lane < nr;
     int row = 0;
@@ -143,10 +122,10 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
 #pragma unroll
         for (int k = 0; k < kTprMax; ++k) xv[k] = (cols[k] >= 0) ? ld_relaxed_val(x + cols[k]) : T(0);
         // Warp-converged loop; each lane publishes as soon as its own row is
-        // ready (not when the chunk's slowest lane is).  Rows with more than
-        // lazy_w dependencies poll lazily (reload_pending_lazy; off by default).
+        // ready (not when the chunk's slowest lane is).  Every pending value is
+        // re-polled each round (polling only the last one measured slower with
+        // one CTA per SM: cfg4 26.8 vs 31.2 ms, cfg3 2.46 vs 2.91 ms).
         bool done = !act;
-        unsigned it = 0;
         for (;;) {
             if (!done && !pending_any<T, kTprMax>(cols, xv)) {
 #pragma unroll
@@ -158,9 +137,8 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
                 done = true;
             }
             if (__all_sync(0xffffffffu, done)) return;
-            if (sleep_ns > 0) __nanosleep(sleep_ns);
-            if (width <= lazy_w) reload_pending<T, kTprMax>(cols, xv, x);
-            else reload_pending_lazy<T, kTprMax>(cols, xv, x, ++it);
+            __nanosleep(20);
+            reload_pending<T, kTprMax>(cols, xv, x);
         }
     } else {
 #pragma unroll
@@ -251,8 +229,7 @@ template <typename T, bool UNIT, int U>
 __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__ chunks, int nchunks,
                                                    const int32_t *__restrict__ perm, const T *__restrict__ invd,
                                                    const int32_t *__restrict__ ecol, const T *__restrict__ eval,
-                                                   const T *b, T *x, unsigned *ctr, unsigned nwarps_total,
-                                                   int lazy_w, unsigned sleep_ns) {
+                                                   const T *b, T *x, unsigned *ctr, unsigned nwarps_total) {
     const int lane = threadIdx.x & 31;
     unsigned long long *tp = g_tpub;         // debug trace (read once)
     for (;;) {
@@ -262,7 +239,7 @@ __global__ void __launch_bounds__(kThreads) k_self(const ChunkDesc *__restrict__
         if ((int)t >= nchunks) break;
         const ChunkDesc cd = chunks[t];
         if (!chunk_wpr(cd.meta))
-            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp, lazy_w, sleep_ns);
+            tpr_chunk<T, UNIT, true>(cd, lane, perm, invd, ecol, eval, b, x, tp);
         else
             wpr_row<T, UNIT, true, U>(cd, lane, perm, invd, ecol, eval, b, x, tp);
     }
@@ -356,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__re
                                                       const int32_t *__restrict__ mr_ptr,
                                                       const int32_t *__restrict__ mr_col,
                                                       const T *__restrict__ mr_val, const T *b, T *x, int nrhs,
-                                                      unsigned *ctr, unsigned nwarps_total) {
+                                                      int64_t ld, unsigned *ctr, unsigned nwarps_total) {
     constexpr int RPW = 32 / W;               // rows per warp
     constexpr int DB = 8;                     // dependency loads in flight per lane
     const int lane = threadIdx.x & 31;
@@ -371,7 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__re
             const int row = perm[p];
             const T di = invd[p];
             const int e0 = mr_ptr[p], e1 = mr_ptr[p + 1];
-            T acc = ld_cg(b + (int64_t)row * nrhs + c);
+            T acc = ld_cg(b + (int64_t)row * ld + c);
             for (int k0 = e0; k0 < e1; k0 += DB) {
                 int cj[DB];
                 T a[DB], v[DB];
@@ -381,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__re
                     a[u] = k0 + u < e1 ? mr_val[k0 + u] : T(0);
                 }
 #pragma unroll
-                for (int u = 0; u < DB; ++u) v[u] = cj[u] >= 0 ? ld_relaxed_val(x + (int64_t)cj[u] * nrhs + c) : T(0);
+                for (int u = 0; u < DB; ++u) v[u] = cj[u] >= 0 ? ld_relaxed_val(x + (int64_t)cj[u] * ld + c) : T(0);
                 for (;;) {
                     bool pend = false;
 #pragma unroll
@@ -390,13 +367,13 @@ __global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__re
                     __nanosleep(20);
 #pragma unroll
                     for (int u = 0; u < DB; ++u)
-                        if (cj[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + (int64_t)cj[u] * nrhs + c);
+                        if (cj[u] >= 0 && Sentinel<T>::is(v[u])) v[u] = ld_relaxed_val(x + (int64_t)cj[u] * ld + c);
                 }
 #pragma unroll
                 for (int u = 0; u < DB; ++u)
                     if (cj[u] >= 0) acc = fnma(a[u], v[u], acc);
             }
-            st_relaxed_val(x + (int64_t)row * nrhs + c, Sentinel<T>::scrub(finish<T, UNIT>(acc, di)));
+            st_relaxed_val(x + (int64_t)row * ld + c, Sentinel<T>::scrub(finish<T, UNIT>(acc, di)));
         }
         __syncwarp();
     }
@@ -409,161 +386,23 @@ __global__ void __launch_bounds__(kThreads) k_mrhs_vf(int n, const int32_t *__re
     }
 }
 
-sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes);
+sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes, cudaStream_t s);
+// nrhs <= 16 columns (kVfMax): one launch; the caller handles the in-place copy
 template <typename T, bool UNIT>
-sptrsv_status_t launch_mrhs_vf(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
-    const size_t elems = (size_t)h->n * nrhs;
-    if ((const void *)b == (const void *)x) {     // in place: keep b aside, x becomes the flag array
-        sptrsv_status_t st = ensure_scratch(h, elems * sizeof(T));
-        if (st != SPTRSV_SUCCESS) return st;
-        SPTRSV_CUDA(cudaMemcpyAsync(h->d_scratch, b, elems * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        b = (const T *)h->d_scratch;
+sptrsv_status_t launch_mrhs_vf(sptrsv_handle_t h, const T *b, T *x, int ncols, int64_t ld, cudaStream_t s) {
+    auto kern = ncols <= 2 ? k_mrhs_vf<T, UNIT, 2> : ncols <= 4 ? k_mrhs_vf<T, UNIT, 4>
+              : ncols <= 8 ? k_mrhs_vf<T, UNIT, 8> : k_mrhs_vf<T, UNIT, 16>;
+    // 4 CTAs per SM (occupancy permitting), computed once per handle
+    if (h->vf_grid == 0) {
+        int per_sm = 0;
+        SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mrhs_vf<T, UNIT, 16>, kThreads, 0));
+        h->vf_grid = std::max(1, std::min(per_sm, 4)) * h->num_sms;
     }
-    k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)elems);
-    auto kern = nrhs <= 2 ? k_mrhs_vf<T, UNIT, 2> : nrhs <= 4 ? k_mrhs_vf<T, UNIT, 4>
-              : nrhs <= 8 ? k_mrhs_vf<T, UNIT, 8> : nrhs <= 16 ? k_mrhs_vf<T, UNIT, 16> : k_mrhs_vf<T, UNIT, 32>;
-    const char *eg = getenv("SPTRSV_MRHS_VF_GRID");
-    int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0));
-    int grid = std::max(1, std::min(per_sm, 4)) * h->num_sms;
-    if (eg && atoi(eg) > 0) grid = std::min(atoi(eg), std::max(1, per_sm) * h->num_sms);
+    const int grid = h->vf_grid;
     kern<<<grid, kThreads, 0, s>>>(h->n, h->d_perm, (const T *)h->d_invd, h->d_mr_ptr, h->d_mr_col,
-                                   (const T *)h->d_mr_val, b, x, nrhs, h->d_ctr, (unsigned)(grid * (kThreads / 32)));
+                                   (const T *)h->d_mr_val, b, x, ncols, ld, h->d_ctr, (unsigned)(grid * (kThreads / 32)));
     SPTRSV_CUDA(cudaGetLastError());
     return SPTRSV_SUCCESS;
-}
-
-constexpr int kMrG = 4;
-
-template <typename T, bool UNIT, int CPL>
-__global__ void __launch_bounds__(kThreads) k_mrhs(int n, const int32_t *__restrict__ perm, const int32_t *__restrict__ lev,
-                                                   const T *__restrict__ invd,
-                                                   const int32_t *__restrict__ mr_ptr,
-                                                   const int32_t *__restrict__ mr_col, const T *__restrict__ mr_val,
-                                                   const T *b, T *x, int nrhs, int *flags, int epoch, unsigned *ctr,
-                                                   unsigned nwarps_total) {
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned t = 0;
-        if (lane == 0) t = atomicAdd(&ctr[0], (unsigned)kMrG);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if ((int)t >= n) break;
-        int row[kMrG], e0[kMrG], deg[kMrG], col[kMrG];
-        T di[kMrG], val[kMrG];
-        T bv[kMrG][CPL];
-        // independent loads of all G rows first
-#pragma unroll
-        for (int g = 0; g < kMrG; ++g) {
-            const int p = (int)t + g;
-            row[g] = -1;
-            deg[g] = 0;
-            if (p < n) {
-                row[g] = perm[p];
-                di[g] = invd[p];
-                e0[g] = mr_ptr[p];
-                deg[g] = mr_ptr[p + 1] - e0[g];
-                col[g] = lane < deg[g] ? mr_col[e0[g] + lane] : -1;
-                val[g] = lane < deg[g] ? mr_val[e0[g] + lane] : T(0);
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    const int c = lane + 32 * j;
-                    if (c < nrhs) bv[g][j] = ld_cg(b + (int64_t)row[g] * nrhs + c);
-                }
-            }
-        }
-        // concurrent path: all G rows valid, in one level, <= 8 dependencies each
-        // (rows of one level are independent): lane g*8+k polls dependency k of row g
-        bool conc = row[kMrG - 1] >= 0;
-        int lv = conc ? lev[row[0]] : 0;
-#pragma unroll
-        for (int g = 1; g < kMrG; ++g) conc = conc && lev[row[g]] == lv;
-#pragma unroll
-        for (int g = 0; g < kMrG; ++g) conc = conc && deg[g] <= 8;
-        if (conc) {
-            const int gq = lane >> 3, kq = lane & 7;
-            int cq = -1;
-#pragma unroll
-            for (int g = 0; g < kMrG; ++g)
-                if (g == gq && kq < deg[g]) cq = mr_col[e0[g] + kq];
-            if (cq >= 0) {
-                int spins = 0;
-                while (ld_acquire(&flags[cq]) != epoch) {
-                    if (++spins > 4) __nanosleep(32);
-                }
-            }
-            __syncwarp();
-            T acc[kMrG][CPL];
-#pragma unroll
-            for (int g = 0; g < kMrG; ++g)
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) acc[g][j] = bv[g][j];
-#pragma unroll
-            for (int g = 0; g < kMrG; ++g) {
-                for (int k = 0; k < deg[g]; ++k) {
-                    const int ck = __shfl_sync(0xffffffffu, col[g], k);
-                    const T vk = __shfl_sync(0xffffffffu, val[g], k);
-#pragma unroll
-                    for (int j = 0; j < CPL; ++j) {
-                        const int c = lane + 32 * j;
-                        if (c < nrhs) acc[g][j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[g][j]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int g = 0; g < kMrG; ++g)
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    const int c = lane + 32 * j;
-                    if (c < nrhs) x[(int64_t)row[g] * nrhs + c] = finish<T, UNIT>(acc[g][j], di[g]);
-                }
-            __syncwarp();
-#pragma unroll
-            for (int g = 0; g < kMrG; ++g)
-                if (lane == g) st_release(&flags[row[g]], epoch);
-            continue;
-        }
-#pragma unroll
-        for (int g = 0; g < kMrG; ++g) {
-            if (row[g] < 0) break;
-            // wait for the dependencies (lane k polls dependency k)
-            for (int kb = 0; kb < deg[g]; kb += 32) {
-                const int c = (kb == 0) ? col[g] : (kb + lane < deg[g] ? mr_col[e0[g] + kb + lane] : -1);
-                if (c >= 0) {
-                    int spins = 0;
-                    while (ld_acquire(&flags[c]) != epoch) {
-                        if (++spins > 4) __nanosleep(32);
-                    }
-                }
-            }
-            __syncwarp();
-            T acc[CPL];
-#pragma unroll
-            for (int j = 0; j < CPL; ++j) acc[j] = bv[g][j];
-            for (int k = 0; k < deg[g]; ++k) {
-                const int ck = k < 32 ? __shfl_sync(0xffffffffu, col[g], k) : mr_col[e0[g] + k];
-                const T vk = k < 32 ? __shfl_sync(0xffffffffu, val[g], k) : mr_val[e0[g] + k];
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    const int c = lane + 32 * j;
-                    if (c < nrhs) acc[j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[j]);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < CPL; ++j) {
-                const int c = lane + 32 * j;
-                if (c < nrhs) x[(int64_t)row[g] * nrhs + c] = finish<T, UNIT>(acc[j], di[g]);
-            }
-            __syncwarp();
-            if (lane == 0) st_release(&flags[row[g]], epoch);
-        }
-    }
-    if (lane == 0) {
-        unsigned e = atomicAdd(&ctr[1], 1u);
-        if (e == nwarps_total - 1) {
-            ctr[0] = 0;
-            ctr[1] = 0;
-        }
-    }
 }
 
 // Level-scheduled multiple right-hand sides (Alg. 1 LEVR over nrhs columns):
@@ -582,7 +421,7 @@ template <typename T, int CPL>
 __device__ __forceinline__ void mr_load(MrRow<T, CPL> &R, int p, int lane, const int32_t *__restrict__ perm,
                                         const T *__restrict__ invd, const int32_t *__restrict__ mr_ptr,
                                         const int32_t *__restrict__ mr_col, const T *__restrict__ mr_val, const T *b,
-                                        int nrhs) {
+                                        int nrhs, int64_t ld) {
     R.row = perm[p];
     R.di = invd[p];
     R.e0 = mr_ptr[p];
@@ -592,13 +431,13 @@ __device__ __forceinline__ void mr_load(MrRow<T, CPL> &R, int p, int lane, const
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
         const int c = lane + 32 * j;
-        if (c < nrhs) R.bv[j] = ld_cg(b + (int64_t)R.row * nrhs + c);
+        if (c < nrhs) R.bv[j] = ld_cg(b + (int64_t)R.row * ld + c);
     }
 }
 
 template <typename T, bool UNIT, int CPL>
 __device__ __forceinline__ void mr_solve(const MrRow<T, CPL> &R, int lane, const int32_t *__restrict__ mr_col,
-                                         const T *__restrict__ mr_val, T *x, int nrhs) {
+                                         const T *__restrict__ mr_val, T *x, int nrhs, int64_t ld) {
     // the x rows of the first kBatch dependencies are loaded together (one
     // memory latency instead of one per dependency); the FMAs then run in
     // storage order, as before
@@ -613,7 +452,7 @@ __device__ __forceinline__ void mr_solve(const MrRow<T, CPL> &R, int lane, const
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
             const int c = lane + 32 * j;
-            xv[k][j] = (k < R.deg && c < nrhs) ? ld_cg(x + (int64_t)ck * nrhs + c) : T(0);
+            xv[k][j] = (k < R.deg && c < nrhs) ? ld_cg(x + (int64_t)ck * ld + c) : T(0);
         }
     }
 #pragma unroll
@@ -630,13 +469,13 @@ __device__ __forceinline__ void mr_solve(const MrRow<T, CPL> &R, int lane, const
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
             const int c = lane + 32 * j;
-            if (c < nrhs) acc[j] = fnma(vk, ld_cg(x + (int64_t)ck * nrhs + c), acc[j]);
+            if (c < nrhs) acc[j] = fnma(vk, ld_cg(x + (int64_t)ck * ld + c), acc[j]);
         }
     }
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
         const int c = lane + 32 * j;
-        if (c < nrhs) x[(int64_t)R.row * nrhs + c] = finish<T, UNIT>(acc[j], R.di);
+        if (c < nrhs) x[(int64_t)R.row * ld + c] = finish<T, UNIT>(acc[j], R.di);
     }
 }
 
@@ -652,14 +491,14 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
                                                          const int32_t *__restrict__ mr_ptr,
                                                          const int32_t *__restrict__ mr_col,
                                                          const T *__restrict__ mr_val, const T *b, T *x, int nrhs,
-                                                         unsigned long long *bar, unsigned long long bar_base) {
+                                                         int64_t ld, unsigned long long *bar, unsigned long long bar_base) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     MrRow<T, CPL> pre;
     int have = 0;
     if (nlev > 0 && ilev[0] + gw < ilev[1]) {
-        mr_load(pre, ilev[0] + gw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+        mr_load(pre, ilev[0] + gw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs, ld);
         have = 1;
     }
     for (int l = 0; l < nlev; ++l) {
@@ -669,8 +508,8 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
         for (int p = p0 + gw; have; p += nw) {
             MrRow<T, CPL> nxt;
             const bool more = p + nw < p1;
-            if (more) mr_load(nxt, p + nw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
-            mr_solve<T, UNIT, CPL>(pre, lane, mr_col, mr_val, x, nrhs);
+            if (more) mr_load(nxt, p + nw, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs, ld);
+            mr_solve<T, UNIT, CPL>(pre, lane, mr_col, mr_val, x, nrhs, ld);
             if (!more) break;
             pre = nxt;
         }
@@ -678,78 +517,12 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
             have = 0;
             const int q = ilev[l + 1] + gw;
             if (q < ilev[l + 2]) {
-                mr_load(pre, q, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs);
+                mr_load(pre, q, lane, perm, invd, mr_ptr, mr_col, mr_val, b, nrhs, ld);
                 have = 1;
             }
             grid_barrier(bar, bar_base + (unsigned long long)(l + 1) * gridDim.x);
         }
     }
-}
-
-// Multi-RHS over the BLOCK partition's CTAs (tile_mrhs_build, block.cu): CTA c
-// walks its non-empty levels in order; within a level its warps take rows
-// (lanes over right-hand sides, the next row's metadata and b loaded before
-// the current row is solved), __syncthreads, then thread 0 publishes the next
-// level it will work on (release).  Before a level l, one thread per producer
-// CTA waits (acquire) until that CTA's counter reaches l: every dependency of
-// a level-l row has a lower level, so no grid-wide barrier is
-// needed and a CTA runs ahead of the ones that do not feed it.
-constexpr int kTileThreads = 512;
-template <typename T, bool UNIT, int CPL>
-__global__ void __launch_bounds__(kTileThreads, 1)
-    k_tile_mrhs(int nlev, const int32_t *__restrict__ off, const int32_t *__restrict__ dptr,
-                const int32_t *__restrict__ dl, unsigned long long *done, unsigned long long base,
-                const int32_t *__restrict__ perm, const T *__restrict__ invd, const int32_t *__restrict__ ptr,
-                const int32_t *__restrict__ col, const T *__restrict__ val, const T *b, T *x, int nrhs) {
-    const int c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int32_t *co = off + (size_t)c * nlev;        // co[l] .. co[l+1]: positions of (c, l)
-    auto next_level = [&](int l) {                      // first non-empty level >= l (nlev if none)
-        while (l < nlev && co[l] == co[l + 1]) ++l;
-        return l;
-    };
-    int l = next_level(0);
-    if (threadIdx.x == 0) st_release_u64(&done[c], base + (unsigned long long)l);
-    const int d0 = dptr[c], nd = dptr[c + 1] - d0;
-    while (l < nlev) {
-        for (int q = threadIdx.x; q < nd; q += blockDim.x) {
-            const unsigned long long *f = &done[dl[d0 + q]];
-            const unsigned long long target = base + (unsigned long long)l;
-            while (ld_acquire_u64(f) < target) {
-            }
-        }
-        __syncthreads();
-        const int p1 = co[l + 1];
-        int p = co[l] + warp;
-        if (p < p1) {
-            MrRow<T, CPL> cur;
-            mr_load(cur, p, lane, perm, invd, ptr, col, val, b, nrhs);
-            for (;; p += nw) {
-                MrRow<T, CPL> nxt;
-                const bool more = p + nw < p1;
-                if (more) mr_load(nxt, p + nw, lane, perm, invd, ptr, col, val, b, nrhs);
-                mr_solve<T, UNIT, CPL>(cur, lane, col, val, x, nrhs);
-                if (!more) break;
-                cur = nxt;
-            }
-        }
-        __syncthreads();
-        l = next_level(l + 1);
-        if (threadIdx.x == 0) st_release_u64(&done[c], base + (unsigned long long)l);
-    }
-}
-
-template <typename T, bool UNIT, int CPL>
-sptrsv_status_t launch_tile_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
-    BlockPlan &B = h->block;
-    const int nlev = h->info.nlev;
-    unsigned long long base = B.tm_base;
-    void *args[] = {(void *)&nlev, (void *)&B.d_tm_off, (void *)&B.d_tm_dptr, (void *)&B.d_tm_dl,
-                    (void *)&B.d_tm_done, (void *)&base, (void *)&B.d_tm_perm, (void *)&B.d_tm_invd,
-                    (void *)&B.d_tm_ptr, (void *)&B.d_tm_col, (void *)&B.d_tm_val, (void *)&b, (void *)&x,
-                    (void *)&nrhs};
-    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_tile_mrhs<T, UNIT, CPL>, B.tm_K, kTileThreads, args, 0, s));
-    B.tm_base += (unsigned long long)nlev + 1;
-    return SPTRSV_SUCCESS;
 }
 
 // per-position CSR of the referenced strict triangle (multi-RHS layout)
@@ -788,15 +561,16 @@ __global__ void k_mr_fill(int nchunks, const ChunkDesc *__restrict__ chunks, con
     }
 }
 
-sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes) {
+// Scratch buffer of the handle (copy of b for in-place value-as-flag solves).
+// Grown on demand; the old buffer is released after `s` drains (stream-ordered).
+sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes, cudaStream_t s) {
     if (h->scratch_bytes >= bytes) return SPTRSV_SUCCESS;
     if (h->d_scratch) {
-        SPTRSV_CUDA(cudaDeviceSynchronize());
-        cudaFree(h->d_scratch);
+        SPTRSV_CUDA(cudaFreeAsync(h->d_scratch, s));
         h->d_scratch = nullptr;
         h->scratch_bytes = 0;
     }
-    SPTRSV_CUDA(cudaMalloc(&h->d_scratch, bytes));
+    SPTRSV_CUDA(cudaMallocAsync(&h->d_scratch, bytes, s));
     h->scratch_bytes = bytes;
     return SPTRSV_SUCCESS;
 }
@@ -829,33 +603,13 @@ sptrsv_status_t build_mr(sptrsv_handle_t h, cudaStream_t s) {
 }
 
 template <typename T, bool UNIT, int CPL>
-sptrsv_status_t launch_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
-    static int grid = 0;
-    if (grid == 0) {
-        int per_sm = 0;
-        SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mrhs<T, UNIT, CPL>, kThreads, 0));
-        grid = std::max(1, per_sm) * h->num_sms;
-        const char *eg = getenv("SPTRSV_MRHS_GRID");      // tuning: absolute CTA count
-        if (eg && atoi(eg) > 0) grid = std::min(grid, atoi(eg));
-    }
-    k_mrhs<T, UNIT, CPL><<<grid, kThreads, 0, s>>>(h->n, h->d_perm, h->d_lev, (const T *)h->d_invd, h->d_mr_ptr,
-                                                   h->d_mr_col,
-                                                   (const T *)h->d_mr_val, b, x, nrhs, h->d_flags, h->epoch,
-                                                   h->d_ctr, (unsigned)(grid * (kThreads / 32)));
-    SPTRSV_CUDA(cudaGetLastError());
-    return SPTRSV_SUCCESS;
-}
-
-template <typename T, bool UNIT, int CPL>
-sptrsv_status_t launch_level_mrhs(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
+sptrsv_status_t launch_level_mrhs(sptrsv_handle_t h, const T *b, T *x, int ncols, int64_t ld, cudaStream_t s) {
     const int grid = h->num_sms;
     const int nlev = h->info.nlev;
     void *args[] = {(void *)&h->d_ilev, (void *)&nlev, (void *)&h->d_perm, (void *)&h->d_invd, (void *)&h->d_mr_ptr,
-                    (void *)&h->d_mr_col, (void *)&h->d_mr_val, (void *)&b, (void *)&x, (void *)&nrhs,
+                    (void *)&h->d_mr_col, (void *)&h->d_mr_val, (void *)&b, (void *)&x, (void *)&ncols, (void *)&ld,
                     (void *)&h->d_bar, (void *)&h->bar_base};
-    const char *emt = getenv("SPTRSV_LEVEL_MRHS_THREADS");
-    const int mt = (emt && atoi(emt) >= 32 && atoi(emt) <= kLevelThreads) ? atoi(emt) / 32 * 32 : kLevelThreads;
-    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level_mrhs<T, UNIT, CPL>, grid, mt, args, 0, s));
+    SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level_mrhs<T, UNIT, CPL>, grid, kLevelThreads, args, 0, s));
     h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
     return SPTRSV_SUCCESS;
 }
@@ -867,103 +621,75 @@ int resident_grid(K kernel, int num_sms) {
     return std::max(1, per_sm) * num_sms;
 }
 
+constexpr int kVfMax = 16;       // widest column block of the value-as-flag multi-RHS kernel
+constexpr int kLevelMax = 128;   // widest column block of the level-scheduled multi-RHS kernel
+
 template <typename T, bool UNIT>
 sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
     if (h->nchunks == 0) return SPTRSV_SUCCESS;
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_LEVEL) {
-        if (h->level_grid == 0) h->level_grid = h->num_sms;
-        const int grid = h->level_grid;
+        const int grid = h->num_sms;
         const int nlev = h->info.nlev;
         void *args[] = {(void *)&h->d_chunks, (void *)&h->d_lev_chunk, (void *)&nlev, (void *)&h->d_perm,
                         (void *)&h->d_invd, (void *)&h->d_ecol, (void *)&h->d_eval, (void *)&b,
                         (void *)&x, (void *)&h->d_bar, (void *)&h->bar_base};
-        const char *elt = getenv("SPTRSV_LEVEL_THREADS");
-        const int lt = (elt && atoi(elt) >= 32 && atoi(elt) <= kLevelThreads1) ? atoi(elt) / 32 * 32 : kLevelThreads1;
-        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, lt, args, 0, s));
+        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_level<T, UNIT>, grid, kLevelThreads1, args, 0, s));
         h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
         return SPTRSV_SUCCESS;
     }
-    if (++h->epoch == INT32_MAX) {   // flag wrap: restart the epoch sequence
-        SPTRSV_CUDA(cudaMemsetAsync(h->d_flags, 0, sizeof(int32_t) * (size_t)h->n, s));
-        h->epoch = 1;
+    const bool level_req = h->algo == SPTRSV_ALGO_LEVEL || h->algo == SPTRSV_ALGO_LEVC;
+    // value-as-flag paths (SELF nrhs = 1, multi-RHS up to 16 columns): x is
+    // the flag array, so an in-place solve keeps b aside first
+    const bool vf = nrhs == 1 || (nrhs <= kVfMax && !level_req);
+    if (vf && (const void *)b == (const void *)x) {
+        const size_t bytes = (size_t)h->n * (size_t)nrhs * sizeof(T);
+        sptrsv_status_t st = ensure_scratch(h, bytes, s);
+        if (st != SPTRSV_SUCCESS) return st;
+        SPTRSV_CUDA(cudaMemcpyAsync(h->d_scratch, b, bytes, cudaMemcpyDeviceToDevice, s));
+        b = (const T *)h->d_scratch;
     }
     if (nrhs == 1) {
-        // WPR batch depth: 8 dependency loads in flight per lane or, with
-        // SPTRSV_WPR_U=16, 16
-        const char *eu = getenv("SPTRSV_WPR_U");
-        const bool u16 = eu && atoi(eu) == 16;
-        auto kself = u16 ? k_self<T, UNIT, 16> : k_self<T, UNIT, 8>;
-        if (h->self_grid == 0 || h->self_u16 != u16) {
+        if (h->self_grid == 0) {
             // one CTA (8 warps) per SM: 74-148 CTAs solve cfg2/3/4 equally fast,
             // 2 CTAs/SM are 10-35% slower -- spinning warps' polls load L2
             // (cfg3 3.92 -> 2.87 ms, cfg2 0.63 -> 0.54 ms, cfg4 34.0 -> 31.1 ms)
-            h->self_grid = std::min(resident_grid(kself, h->num_sms), h->num_sms);
+            h->self_grid = std::min(resident_grid(k_self<T, UNIT, 8>, h->num_sms), h->num_sms);
             // rows with many dependencies (mean >= 8) poll more values per lane:
             // half the SMs' worth of warps is enough and loads L2 less
             // (cfg3, 13 deps/row: 2.47 -> 2.14 ms; cfg4 26.8 -> 26.6 ms; cfg2,
             // 3 deps/row, prefers 148 CTAs: 0.54 vs 0.62 ms)
             const int64_t strict = h->info.nnz_used;          // referenced strict entries
             if (h->n > 0 && strict >= 8 * (int64_t)h->n) h->self_grid = std::max(1, h->self_grid / 2);
-            const char *ec = getenv("SPTRSV_SELF_CPS");      // CTAs per SM (fewer spinning warps)
-            if (ec && atoi(ec) > 0) h->self_grid = std::min(h->self_grid, atoi(ec) * h->num_sms);
-            const char *eg = getenv("SPTRSV_SELF_GRID");     // absolute CTA count (tuning)
-            if (eg && atoi(eg) > 0) h->self_grid = std::min(h->self_grid, atoi(eg));
-            h->self_u16 = u16;
         }
         const int grid = h->self_grid;
-        // TPR rows wider than lazy_w poll lazily (SPTRSV_TPR_LAZY_W); default
-        // never: with one CTA per SM, polling every pending dependency is faster
-        // (cfg4 26.8 vs 31.2 ms, cfg3 2.46 vs 2.91 ms with lazy_w = 12)
-        const char *elw = getenv("SPTRSV_TPR_LAZY_W");
-        const int lazy_w = elw ? atoi(elw) : kTprMax;
-        const char *esl = getenv("SPTRSV_SELF_SLEEP");      // ns between TPR polls
-        const unsigned sleep_ns = esl ? (unsigned)atoi(esl) : 20u;
-        if ((const void *)b == (const void *)x) {   // in place: keep b aside, x becomes the flag array
-            sptrsv_status_t st = ensure_scratch(h, (size_t)h->n * sizeof(T));
-            if (st != SPTRSV_SUCCESS) return st;
-            SPTRSV_CUDA(cudaMemcpyAsync(h->d_scratch, b, (size_t)h->n * sizeof(T), cudaMemcpyDeviceToDevice, s));
-            b = (const T *)h->d_scratch;
-        }
         k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n);
-        kself<<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
-                                                  h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
-                                                  (unsigned)(grid * (kThreads / 32)), lazy_w, sleep_ns);
-    } else {
-        if (!h->mr_built) {
-            sptrsv_status_t st = build_mr<T>(h, s);
-            if (st != SPTRSV_SUCCESS) return st;
-        }
-        // CTA-tile multi-RHS (k_tile_mrhs) on request (env SPTRSV_MRHS_TILE=1):
-        // on cfg5 the level-scheduled multi-RHS kernel is faster (profiles/)
-        const char *ev = getenv("SPTRSV_MRHS_TILE");
-        const bool tiled = (h->algo == SPTRSV_ALGO_BLOCK || h->algo == SPTRSV_ALGO_TILE) && ev && *ev == '1';
-        if (tiled && !h->block.tm_built && h->block.built && h->block.grid_nx > 0) {
-            sptrsv_status_t st = tile_mrhs_build(h, s);
-            if (st != SPTRSV_SUCCESS) return st;
-        }
-        if (tiled && h->block.tm_built) {
-            if (nrhs <= 32) return launch_tile_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
-            if (nrhs <= 64) return launch_tile_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
-            if (nrhs <= 128) return launch_tile_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
-            return SPTRSV_ERR_NOT_SUPPORTED;
-        }
-        // SELF / SLFC: self-scheduled multi-RHS; LEVEL / LEVC / BLOCK / TILE: level-scheduled
-        const bool lv = h->algo != SPTRSV_ALGO_SELF && h->algo != SPTRSV_ALGO_SLFC;
-        // value-as-flag multi-RHS for nrhs <= 16 (cfg5 ranks of 4 / 8 GPUs: 16 RHS
-        // 1.02 vs 1.73 ms, 8 RHS 0.59 vs 1.72 ms for the level-scheduled kernel;
-        // 32 RHS: 2.02 vs 1.74 ms, so not there), unless LEVEL / LEVC was asked
-        // for; SPTRSV_MRHS_VF=0 disables it, =1 also takes 17..32
-        const char *evf = getenv("SPTRSV_MRHS_VF");
-        const int vf_max = evf ? (*evf == '0' ? 0 : 32) : 16;
-        const bool level_req = h->algo == SPTRSV_ALGO_LEVEL || h->algo == SPTRSV_ALGO_LEVC;
-        if (nrhs <= vf_max && !level_req) return launch_mrhs_vf<T, UNIT>(h, b, x, nrhs, s);
-        if (nrhs <= 32) return lv ? launch_level_mrhs<T, UNIT, 1>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 1>(h, b, x, nrhs, s);
-        if (nrhs <= 64) return lv ? launch_level_mrhs<T, UNIT, 2>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 2>(h, b, x, nrhs, s);
-        if (nrhs <= 128) return lv ? launch_level_mrhs<T, UNIT, 4>(h, b, x, nrhs, s) : launch_mrhs<T, UNIT, 4>(h, b, x, nrhs, s);
-        // wider: independent column blocks of 128 (each column's arithmetic is unchanged)
-        return SPTRSV_ERR_NOT_SUPPORTED;
+        k_self<T, UNIT, 8><<<grid, kThreads, 0, s>>>(h->d_chunks, h->nchunks, h->d_perm, (const T *)h->d_invd,
+                                                     h->d_ecol, (const T *)h->d_eval, b, x, h->d_ctr,
+                                                     (unsigned)(grid * (kThreads / 32)));
+        SPTRSV_CUDA(cudaGetLastError());
+        return SPTRSV_SUCCESS;
     }
-    SPTRSV_CUDA(cudaGetLastError());
+    if (!h->mr_built) {          // first multi-RHS solve on the handle: builds the per-position CSR (syncs)
+        sptrsv_status_t st = build_mr<T>(h, s);
+        if (st != SPTRSV_SUCCESS) return st;
+    }
+    // value-as-flag multi-RHS for nrhs <= 16 (cfg5 ranks of 4 / 8 GPUs: 16 RHS
+    // 1.02 vs 1.73 ms, 8 RHS 0.59 vs 1.72 ms for the level-scheduled kernel;
+    // 32 RHS: 2.02 vs 1.74 ms), unless LEVEL / LEVC was asked for
+    if (vf) {
+        k_prefill<T><<<h->num_sms * 4, 512, 0, s>>>(x, (int64_t)h->n * nrhs);
+        return launch_mrhs_vf<T, UNIT>(h, b, x, nrhs, nrhs, s);
+    }
+    // level-scheduled, in independent column blocks of <= 128 (each column's
+    // arithmetic is the same whatever block it is in)
+    for (int c0 = 0; c0 < nrhs; c0 += kLevelMax) {
+        const int nc = std::min(kLevelMax, nrhs - c0);
+        sptrsv_status_t st;
+        if (nc <= 32) st = launch_level_mrhs<T, UNIT, 1>(h, b + c0, x + c0, nc, nrhs, s);
+        else if (nc <= 64) st = launch_level_mrhs<T, UNIT, 2>(h, b + c0, x + c0, nc, nrhs, s);
+        else st = launch_level_mrhs<T, UNIT, 4>(h, b + c0, x + c0, nc, nrhs, s);
+        if (st != SPTRSV_SUCCESS) return st;
+    }
     return SPTRSV_SUCCESS;
 }
 
@@ -976,7 +702,6 @@ sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s) {
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s) {
     if (nrhs == 1 && (h->algo == SPTRSV_ALGO_SLFC || h->algo == SPTRSV_ALGO_LEVC)) return column_solve(h, b, x, s);
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_BLOCK) return block_solve(h, b, x, s);
-    if (nrhs == 1 && h->algo == SPTRSV_ALGO_TILE) return tile_solve(h, b, x, s);
     if (h->dtype == SPTRSV_F64) {
         return h->diag == SPTRSV_UNIT ? launch<double, true>(h, (const double *)b, (double *)x, nrhs, s)
                                       : launch<double, false>(h, (const double *)b, (double *)x, nrhs, s);

@@ -21,8 +21,8 @@ LIB_PATH = _build.LIB
 LOWER, UPPER = 0, 1
 NON_UNIT, UNIT = 0, 1
 F64, F32 = 0, 1
-ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_TILE, ALGO_SLFC, ALGO_LEVC = 0, 1, 2, 3, 4, 5, 6
-ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK, "auto": ALGO_AUTO, "tile": ALGO_TILE,
+ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_SLFC, ALGO_LEVC = 0, 1, 2, 3, 5, 6
+ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK, "auto": ALGO_AUTO,
          "slfc": ALGO_SLFC, "levc": ALGO_LEVC}
 UPLO = {"lower": LOWER, "upper": UPPER}
 DIAG = {"non_unit": NON_UNIT, "unit": UNIT}
@@ -69,6 +69,8 @@ def _load():
     lib.sptrsv_get_levels.argtypes = [vp, vp, vp, vp]
     lib.sptrsv_get_dep_counts.restype = ctypes.c_int
     lib.sptrsv_get_dep_counts.argtypes = [vp, vp]
+    lib.sptrsv_get_solve_status.restype = ctypes.c_int
+    lib.sptrsv_get_solve_status.argtypes = [vp]
     lib.sptrsv_status_string.restype = ctypes.c_char_p
     lib.sptrsv_status_string.argtypes = [ctypes.c_int]
     lib.sptrsv_last_cuda_error.restype = ctypes.c_char_p
@@ -134,6 +136,10 @@ def sptrsv_get_dep_counts(handle, dp_ptr) -> int:
     return _lib.sptrsv_get_dep_counts(handle, dp_ptr)
 
 
+def sptrsv_get_solve_status(handle) -> int:
+    return _lib.sptrsv_get_solve_status(handle)
+
+
 # ------------------------------------------------------------- wrapper
 def _stream_ptr(stream):
     import torch
@@ -164,6 +170,14 @@ class TriangularSolver:
         for t in (rowptr, colidx):
             if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
                 raise TypeError("rowptr/colidx must be contiguous int32 CUDA tensors")
+        if rowptr.numel() != self.n + 1:
+            raise ValueError(f"rowptr must have n + 1 = {self.n + 1} entries")
+        nnz = int(rowptr[-1].item()) if self.n > 0 else 0
+        if colidx.numel() < nnz:
+            raise ValueError(f"colidx has {colidx.numel()} entries, rowptr[n] = {nnz}")
+        if vals is not None:
+            if not vals.is_cuda or not vals.is_contiguous() or vals.numel() < nnz:
+                raise ValueError(f"vals must be a contiguous CUDA tensor of >= rowptr[n] = {nnz} values")
         st, h = sptrsv_analyze(self.n, _dptr(rowptr), _dptr(colidx), _dptr(vals), UPLO[uplo], DIAG[diag],
                                dtype, _stream_ptr(stream))
         self.handle = h
@@ -210,19 +224,38 @@ class TriangularSolver:
         import torch
         if b.dtype != self.torch_dtype or not b.is_cuda or not b.is_contiguous():
             raise TypeError(f"b must be a contiguous {self.torch_dtype} CUDA tensor")
+        if b.dim() not in (1, 2) or b.shape[0] != self.n:
+            raise ValueError(f"b must have shape ({self.n},) or ({self.n}, nrhs), got {tuple(b.shape)}")
         nrhs = 1 if b.dim() == 1 else b.shape[1]
         if x is None:
             x = torch.empty_like(b)
+        elif (x.shape != b.shape or x.dtype != b.dtype or x.device != b.device or not x.is_contiguous()):
+            raise TypeError("x must be a contiguous tensor with b's shape, dtype and device")
         st = sptrsv_solve(self.handle, _dptr(b), _dptr(x), nrhs, _stream_ptr(stream))
         if st != 0:
             raise SptrsvError(st, "sptrsv_solve")
         return x
 
+    def solve_status(self) -> str:
+        """Synchronizes; "SUCCESS", or "TIMEOUT" if the last (BLOCK) solve gave up a spin wait."""
+        return STATUS_NAMES.get(sptrsv_get_solve_status(self.handle), "UNKNOWN")
+
     def solve_host(self, b, x=None, stream=None):
         """The same solve on HOST arrays (numpy or CPU tensors); copies are inside the call."""
+        want = np.float64 if self.torch_dtype.is_floating_point and self.torch_dtype.itemsize == 8 else np.float32
+        for name, a in (("b", b), ("x", x)):
+            if a is None:
+                continue
+            arr = a if isinstance(a, np.ndarray) else a.numpy()
+            if arr.dtype != want or not arr.flags["C_CONTIGUOUS"]:
+                raise TypeError(f"{name} must be a C-contiguous {np.dtype(want).name} host array")
+        if b.ndim not in (1, 2) or b.shape[0] != self.n:
+            raise ValueError(f"b must have shape ({self.n},) or ({self.n}, nrhs), got {tuple(b.shape)}")
         nrhs = 1 if b.ndim == 1 else b.shape[1]
         if x is None:
             x = np.empty_like(b) if isinstance(b, np.ndarray) else b.new_empty(b.shape)
+        elif tuple(x.shape) != tuple(b.shape):
+            raise ValueError("x must have b's shape")
         bp = b.ctypes.data_as(ctypes.c_void_p) if isinstance(b, np.ndarray) else ctypes.c_void_p(b.data_ptr())
         xp = x.ctypes.data_as(ctypes.c_void_p) if isinstance(x, np.ndarray) else ctypes.c_void_p(x.data_ptr())
         st = sptrsv_solve_host(self.handle, bp, xp, nrhs, _stream_ptr(stream))

@@ -36,18 +36,18 @@ def relerr(x, ref):
     return float(np.abs(x - ref).max() / den) if ref.size else 0.0
 
 
-def watchdog_clear(S):
-    """BLOCK's spin watchdog (debug hook): 1 means a wait gave up -- a scheduling bug."""
-    import ctypes
-    return ctypes.CDLL(S.LIB_PATH).sptrsv_dbg_watchdog() == 0
+def avg_deps(m, uplo="lower"):
+    rows = np.repeat(np.arange(m.n), np.diff(m.rowptr))
+    strict = (m.colidx < rows) if uplo == "lower" else (m.colidx > rows)
+    return strict.sum() / max(m.n, 1)
 
 
 def gpu_solve(S, m, b, uplo="lower", diag="non_unit", dtype=np.float64, algo="self", solver=None):
     solver = solver or S.from_csr(m, uplo, diag, dtype, algo)
     bt = torch.from_numpy(np.ascontiguousarray(b, dtype=dtype)).cuda()
     x = solver.solve(bt)
-    torch.cuda.synchronize()
-    assert watchdog_clear(S)
+    # every solve must complete: BLOCK's per-solve watchdog never fires on valid input
+    assert solver.solve_status() == "SUCCESS"
     return x.cpu().numpy(), solver
 
 
@@ -156,6 +156,12 @@ def test_solve_random_small(S, uplo, diag, dtype, algo):
             m.vals[off] *= 0.5 / max(1.0, np.diff(m.rowptr).max())
         b = workloads.rhs(n, 1, seed=seed)[:, 0]
         ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, diag, dtype=dtype)
+        if algo == "block" and avg_deps(m, uplo) > 3:
+            # BLOCK refuses natural partitions with > 3 dependencies per row on average
+            with pytest.raises(S.SptrsvError) as e:
+                S.from_csr(m, uplo, diag, dtype, algo)
+            assert e.value.name == "NOT_SUPPORTED"
+            continue
         x, _ = gpu_solve(S, m, b, uplo, diag, dtype, algo)
         assert relerr(x, ref) <= TOL[dtype], (seed, n)
 
@@ -240,9 +246,8 @@ def test_multi_rhs_small(S, nrhs, algo):
 
 @pytest.mark.parametrize("nrhs", [2, 17, 64, 100])
 @pytest.mark.parametrize("case", ["7pt_lower", "7pt_upper", "27pt_lower_unit", "5pt_2d"])
-def test_multi_rhs_tiles(S, case, nrhs, monkeypatch):
-    # BLOCK on detected grids: the CTA-tile multi-RHS kernel (producer-CTA waits)
-    monkeypatch.setenv("SPTRSV_MRHS_TILE", "1")
+def test_multi_rhs_grids_block(S, case, nrhs):
+    # BLOCK on detected grids: multi-RHS solves (column blocks, ragged widths)
     if case == "7pt_lower":
         m, uplo, diag = workloads.stencil((24, 20, 12), 7, "lower"), "lower", "non_unit"
     elif case == "7pt_upper":
@@ -339,76 +344,43 @@ def test_invalid_value_and_empty(S):
     assert S.sptrsv_set_algo(sv2.handle, 9) == 1
 
 
-# ------------------------------------------------------------ TILE (CTA tiles, grids)
-TILE_CASES = [((32, 32), 5, "lower"), ((64, 48), 5, "upper"), ((16, 16, 16), 7, "lower"),
-              ((40, 30, 20), 7, "lower"), ((40, 30, 20), 7, "upper"), ((128, 128, 128), 7, "lower")]
+# ------------------------------------------------------------ BLOCK (warp tiles)
+GRID_CASES = [((32, 32), 5, "lower"), ((64, 48), 5, "upper"), ((16, 16, 16), 7, "lower"),
+              ((40, 30, 20), 7, "lower"), ((40, 30, 20), 7, "upper"), ((128, 128, 128), 7, "lower"),
+              ((97, 45, 13), 7, "lower"), ((33, 65), 9, "lower"), ((24, 20, 12), 27, "lower")]
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("dims,pts,uplo", TILE_CASES)
-def test_tile_solve_grids(S, dims, pts, uplo, dtype):
-    m = workloads.stencil(dims, pts, uplo)
-    b = workloads.rhs(m.n, 1, seed=len(dims) * 10 + pts)[:, 0]
-    ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, dtype=dtype)
-    x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="tile")
-    assert sv.info()["algo"] == 4
-    assert relerr(x, ref) <= TOL[dtype]
-    x2, _ = gpu_solve(S, m, b, dtype=dtype, solver=sv)   # run-to-run bitwise (epoch counters advance)
-    assert np.array_equal(x, x2)
-
-
-@pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("uplo", ["lower", "upper"])
-def test_tile_integer_exact_and_in_place(S, uplo, dtype):
-    m = workloads.stencil((40, 30, 20), 7, uplo, diag=8.0)
-    xt = workloads.integer_xtrue(m.n, 1, seed=101)[:, 0]
-    b = oracle.matvec(m, xt, uplo)
-    x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="tile")
-    assert np.array_equal(x.astype(np.float64), xt)
-    bt = torch.from_numpy(b.astype(dtype)).cuda()
-    sv.solve(bt, x=bt)
-    assert np.array_equal(bt.cpu().numpy().astype(np.float64), xt)
-
-
-def test_tile_not_supported_off_grid(S):
-    m = random_triangular_fast(3000, 4.0, 3, "lower")
-    with pytest.raises(S.SptrsvError):
-        S.from_csr(m, algo="tile")
-    sv = S.from_csr(m, algo="auto")                  # auto falls back to SELF off grids
-    assert sv.info()["algo"] == 0
-
-
-# ------------------------------------------------------------ lean BLOCK (k_block1, SPTRSV_BLOCK_LEAN=1)
-LEAN_CASES = TILE_CASES + [((96, 96, 96), 27, "lower")]
-
-
-@pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("dims,pts,uplo", LEAN_CASES)
-def test_lean_block_grids(S, dims, pts, uplo, dtype, monkeypatch):
-    """The one-warp-per-tile kernel: oracle tolerance, run-to-run bitwise, and
-    bitwise equal to the helper kernel (same records, same arithmetic order).
-    27-point rows have more EXT terms than its 4 record entries: overflow lists."""
+@pytest.mark.parametrize("dims,pts,uplo", GRID_CASES)
+def test_block_grids(S, dims, pts, uplo, dtype):
+    """Detected grids (tiles), ragged tile edges, 9- and 27-point rows (more
+    than 3 terms: overflow lists); oracle tolerance, run-to-run bitwise, and
+    bitwise equal to the storage-order multi-RHS kernels column by column."""
     m = workloads.stencil(dims, pts, uplo)
     b = workloads.rhs(m.n, 1, seed=len(dims) * 10 + pts + 1)[:, 0]
     ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, dtype=dtype)
-    x0, _ = gpu_solve(S, m, b, uplo, dtype=dtype, algo="block")
-    monkeypatch.setenv("SPTRSV_BLOCK_LEAN", "1")
     x, sv = gpu_solve(S, m, b, uplo, dtype=dtype, algo="block")
+    assert sv.info()["algo"] == 2 and sv.info()["nblocks"] > 0
     assert relerr(x, ref) <= TOL[dtype]
-    assert np.array_equal(x, x0)
-    x2, _ = gpu_solve(S, m, b, dtype=dtype, solver=sv)
+    x2, _ = gpu_solve(S, m, b, uplo, dtype=dtype, solver=sv)
     assert np.array_equal(x, x2)
+    if m.n <= 200000:                    # storage-order FMA: equal to the multi-RHS columns
+        B2 = np.ascontiguousarray(np.stack([b, b], axis=1)).astype(dtype)
+        X2 = sv.solve(torch.from_numpy(B2).cuda()).cpu().numpy()
+        assert np.array_equal(X2[:, 1], x)
 
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("uplo,diag", [("lower", "non_unit"), ("upper", "unit")])
-def test_lean_block_random_and_integer(S, seed, uplo, diag, monkeypatch):
-    """Natural-order partition (no grid): SMEM/GLOB/overflow EXT terms of every kind."""
-    monkeypatch.setenv("SPTRSV_BLOCK_LEAN", "1")
-    m = random_triangular_fast(2500 + 611 * seed, 3.0 + seed, seed, uplo)
+def test_block_natural_partition_and_integer(S, seed, uplo, diag):
+    """Natural-order partition (no grid): SHFL / SMEM / GLOB / overflow terms
+    of every kind; integer-exact grids bitwise, also in place."""
+    m = random_triangular_fast(2500 + 611 * seed, 1.0 + 0.4 * seed, seed, uplo)
+    assert avg_deps(m, uplo) <= 3
     b = workloads.rhs(m.n, 1, seed=seed)[:, 0]
     ref = oracle.solve(m, b, uplo, diag)
-    x, _ = gpu_solve(S, m, b, uplo, diag, algo="block")
+    x, sv = gpu_solve(S, m, b, uplo, diag, algo="block")
+    assert sv.info()["algo"] == 2
     assert relerr(x, ref) <= 1e-10
     g = workloads.stencil((40, 30, 20), 7, uplo, diag=8.0)
     xt = workloads.integer_xtrue(g.n, 1, seed=101 + seed)[:, 0]
@@ -417,8 +389,39 @@ def test_lean_block_random_and_integer(S, seed, uplo, diag, monkeypatch):
     assert np.array_equal(xg, xt)
     bt = torch.from_numpy(bb).cuda()                    # in place
     sv.solve(bt, x=bt)
-    torch.cuda.synchronize()
+    assert sv.solve_status() == "SUCCESS"
     assert np.array_equal(bt.cpu().numpy(), xt)
+
+
+def test_block_refuses_dense_natural_partition(S):
+    m, p = workloads.config(4, scale=1 / 64)
+    with pytest.raises(S.SptrsvError) as e:
+        S.from_csr(m, p["uplo"], p["diag"], algo="block")
+    assert e.value.name == "NOT_SUPPORTED"
+    assert S.from_csr(m, p["uplo"], p["diag"], algo="auto").info()["algo"] == 0
+
+
+def test_block_watchdog_timeout_then_clean(S):
+    """A BLOCK solve that gives up a spin wait reports TIMEOUT through
+    sptrsv_get_solve_status (per handle, per solve); the next solve is clean."""
+    import ctypes
+    lib = ctypes.CDLL(S.LIB_PATH)
+    lib.sptrsv_dbg_set_timeout_ns.argtypes = [ctypes.c_void_p, ctypes.c_ulonglong]
+    m = chain(200000, sub=-0.5, d=1.0)                   # natural partition: waits on every CTA crossing
+    b = workloads.rhs(m.n, 1, seed=4)[:, 0]
+    sv = S.from_csr(m, algo="block")
+    bt = torch.from_numpy(b).cuda()
+    assert lib.sptrsv_dbg_set_timeout_ns(ctypes.c_void_p(sv.handle), 0) == 0
+    sv.solve(bt)
+    assert sv.solve_status() == "TIMEOUT"
+    assert S.sptrsv_get_solve_status(sv.handle) == 7
+    other = S.from_csr(m, algo="block")                  # another handle is unaffected
+    x, _ = gpu_solve(S, m, b, solver=other)
+    assert lib.sptrsv_dbg_set_timeout_ns(ctypes.c_void_p(sv.handle), 4_000_000_000) == 0
+    x2 = sv.solve(bt)
+    assert sv.solve_status() == "SUCCESS"
+    ref = oracle.solve(m, b)
+    assert relerr(x2.cpu().numpy(), ref) <= 1e-10 and relerr(x, ref) <= 1e-10
 
 
 # ------------------------------------------------------------ column-wise SLFC / LEVC (NEXT-1)
@@ -539,7 +542,6 @@ def test_multi_rhs_value_as_flag(S, nrhs, uplo, diag, dtype):
     sv.solve(Bi, x=Bi)
     torch.cuda.synchronize()
     assert np.array_equal(Bi.cpu().numpy(), X)
-    assert watchdog_clear(S)
 
 
 @pytest.mark.parametrize("uplo", ["lower", "upper"])
