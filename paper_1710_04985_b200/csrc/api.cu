@@ -249,12 +249,13 @@ extern "C" int sptrsv_dbg_block_trace(sptrsv_handle_t h, void *dev_buf, int cap)
     return SPTRSV_SUCCESS;
 }
 
-// BLOCK plan summary for tools: {K, wpc, nsteps, G, nslots, smem, rec_bytes, tile_w, tile_h}
-extern "C" int sptrsv_dbg_block_plan(sptrsv_handle_t h, long long *out9) {
-    if (!h || !out9) return SPTRSV_ERR_INVALID_VALUE;
+// BLOCK plan summary for tools: {K, wpc, nsteps, G, nslots, smem, rec_bytes,
+// tile_w, tile_h, cluster size, cluster x extent, inbound items, gl}
+extern "C" int sptrsv_dbg_block_plan(sptrsv_handle_t h, long long *out13) {
+    if (!h || !out13) return SPTRSV_ERR_INVALID_VALUE;
     const sptrsv::BlockPlan &B = h->block;
-    const long long v[9] = {B.nblocks, B.wpc, B.nsteps, B.G, B.nslots, (long long)B.smem, B.rec_bytes, B.tile_w,
-                            B.tile_h};
-    for (int i = 0; i < 9; ++i) out9[i] = v[i];
+    const long long v[13] = {B.nblocks, B.wpc, B.nsteps, B.G, B.nslots, (long long)B.smem, B.rec_bytes, B.tile_w,
+                             B.tile_h, B.cs, B.csx, B.nitems, B.gl ? 1 : 0};
+    for (int i = 0; i < 13; ++i) out13[i] = v[i];
     return B.built ? SPTRSV_SUCCESS : SPTRSV_ERR_NOT_SUPPORTED;
 }

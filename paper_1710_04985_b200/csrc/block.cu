@@ -76,38 +76,39 @@ constexpr int kSH = 3;                   // terms per record row
 // Two streams per (warp, step), SoA over 32 lanes, 16-byte aligned parts:
 //   ctl  int4 {code0, code1, code2, row}[32]                               512 B
 //        row: -1 on padding lanes
-//   coef T = double: double2 {a0, a1}[32] | double2 {a2, 1/d}[32] | int2 {pub_s, pub_g}[32]   1280 B
-//        T = float : float4 {a0, a1, a2, 1/d}[32] | int2 {pub_s, pub_g}[32]                    768 B
-//        pub_s: shared slot or -1; pub_g: mailbox or -1
+//   coef T = double: double2 {a0, a1}[32] | double2 {a2, 1/d}[32] | int4 pub[32]   1536 B
+//        T = float : float4 {a0, a1, a2, 1/d}[32] | int4 pub[32]                    1024 B
+//        pub = {shared slot, mailbox, remote 0, remote 1} (-1: none); remote =
+//        rank << 24 | slot: a shared slot of another CTA of the cluster (DSMEM)
 // The control stream is read further ahead (b gathers, GLOB prefetch) than
 // the coefficients, so it has the deeper ring.  Every warp's steps are padded
 // to a multiple of UNR with empty steps (no bounds checks in the loop).
 constexpr int kCtlBytes = 512;
 template <typename T> struct Coef;
 template <> struct Coef<double> {
-    static constexpr int BYTES = 1280, PUB = 1024;
+    static constexpr int BYTES = 1536, PUB = 1024;
     double a0, a1, a2, invd;
     __device__ __forceinline__ void load(const unsigned char *r, int lane) {
         const double2 c0 = reinterpret_cast<const double2 *>(r)[lane];
         const double2 c1 = reinterpret_cast<const double2 *>(r + 512)[lane];
         a0 = c0.x; a1 = c0.y; a2 = c1.x; invd = c1.y;
     }
-    __device__ static void put(unsigned char *r, int lane, const double (&a)[3], double invd, int2 pub) {
+    __device__ static void put(unsigned char *r, int lane, const double (&a)[3], double invd, int4 pub) {
         reinterpret_cast<double2 *>(r)[lane] = make_double2(a[0], a[1]);
         reinterpret_cast<double2 *>(r + 512)[lane] = make_double2(a[2], invd);
-        reinterpret_cast<int2 *>(r + PUB)[lane] = pub;
+        reinterpret_cast<int4 *>(r + PUB)[lane] = pub;
     }
 };
 template <> struct Coef<float> {
-    static constexpr int BYTES = 768, PUB = 512;
+    static constexpr int BYTES = 1024, PUB = 512;
     float a0, a1, a2, invd;
     __device__ __forceinline__ void load(const unsigned char *r, int lane) {
         const float4 c = reinterpret_cast<const float4 *>(r)[lane];
         a0 = c.x; a1 = c.y; a2 = c.z; invd = c.w;
     }
-    __device__ static void put(unsigned char *r, int lane, const float (&a)[3], float invd, int2 pub) {
+    __device__ static void put(unsigned char *r, int lane, const float (&a)[3], float invd, int4 pub) {
         reinterpret_cast<float4 *>(r)[lane] = make_float4(a[0], a[1], a[2], invd);
-        reinterpret_cast<int2 *>(r + PUB)[lane] = pub;
+        reinterpret_cast<int4 *>(r + PUB)[lane] = pub;
     }
 };
 
@@ -118,21 +119,21 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 // b(row) DG steps ahead goes to shared memory by cp.async, one commit group
 // per step, so `cp.async.wait_group DG-1` waits for exactly the oldest step's
 // load (register-ring loads would share counting scoreboards and wait for the
-// newest ones too); b also gets an L2 prefetch PB steps ahead.  Values from
-// other CTAs reach shared slots through the CTA's fetcher warp, so a step
-// only reads shared memory, every load one step before its use (stage
-// registers).
+// newest ones too).  Values from other CTAs reach shared slots through the
+// CTA's fetcher warp, so a step only reads shared memory, every load one step
+// before its use (stage registers).  SHFL and NONE codes (< 32, 32) address
+// the zero slots, so the EXT read of every term is one unconditional LDS.
 constexpr int UB = 4;                  // steps per TMA block
 constexpr int NCB = 8, DC = 7;         // control ring (blocks) / TMA lookahead (blocks)
 constexpr int NFB = 4, DF = 3;         // coefficient ring (blocks) / TMA lookahead (blocks)
 constexpr int DP = 12;                 // L2 prefetch lookahead (blocks), both streams
-constexpr int DG = 8;                  // b(row) and GLOB loads in flight (steps): cp.async landing rings
-constexpr int PB = 16;                 // b(row) L2 prefetch distance (steps)
+constexpr int DG = 16;                 // b(row) loads in flight (steps): cp.async landing ring
 constexpr int UNR = 8;                 // main-loop unroll = per-warp step padding
-constexpr int XB = (PB + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
+constexpr int XB = (DG + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
 constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
-static_assert(NCB > DC && NFB > DF && UNR % DG == 0 && UNR % UB == 0, "ring shapes");
-static_assert((PB + 1 + UB - 1) / UB + 2 <= DC, "control records must land before their b prefetch");
+constexpr int kZeroSlots = 64;         // shared slots 0..63 hold 0.0: the EXT read of a non-EXT term
+static_assert(NCB > DC && NFB > DF && DG % UNR == 0 && UNR % UB == 0, "ring shapes");
+static_assert((DG + 1 + UB - 1) / UB + 2 <= DC, "control records must land before their b gather");
 static_assert((NCB * UB) % UNR == 0 && (NFB * UB) % UNR == 0, "ring offsets advance by whole iterations");
 
 // per compute warp: control ring, coefficient ring, b landing [DG][32], barriers
@@ -191,15 +192,17 @@ __global__ void k_grid_check(int n, int nx, int ny, const int32_t *__restrict__ 
 }
 
 // (x, y) tiles of tw x th columns; CTA = wx x wy tiles; unit = cta * wpc + warp.
+// CTAs are numbered by clusters of csx x csy CTAs (rank = position inside).
 // UPPER numbers the CTAs backwards so that every dependency points to a
 // lower-numbered CTA in both cases.
 __global__ void k_part_tiles(int n, int nx, int ny, int tw, int th, int wx, int wy, int cxn, int K, int upper,
-                             int32_t *unit) {
+                             int csx, int csy, int32_t *unit) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int x = i % nx, y = (i / nx) % ny;
     const int txi = x / tw, tyi = y / th;
-    int cta = (tyi / wy) * cxn + txi / wx;
+    const int cx = txi / wx, cy = tyi / wy;
+    int cta = ((cy / csy) * (cxn / csx) + cx / csx) * (csx * csy) + (cy % csy) * csx + cx % csx;
     int w = (tyi % wy) * wx + (txi % wx);
     if (upper) {
         cta = K - 1 - cta;
@@ -306,56 +309,102 @@ __global__ void k_need(int n, int wpc, const int32_t *__restrict__ tri_ptr, cons
         const int j = tri_col[k];
         const int uj = unit[j], pj = pos[j];
         if (dep_shfl(ui, si, uj, step_of[pj])) continue;
-        if (uj / wpc == ui / wpc && !ns) {
-            atomicOr(&need[pj], 1);
-        } else {
-            atomicOr(&need[pj], 2);
-            ++cross;
-        }
+        if (uj / wpc == ui / wpc && !ns) atomicOr(&need[pj], 1);
+        else ++cross;
     }
     icnt[pi] = cross;
 }
 
-// inbound items of CROSS dependencies, numbered by (position, storage order):
-// key (consumer CTA, level), source mailbox
-__global__ void k_items(int n, int nlev, int wpc, const int32_t *__restrict__ bperm, const int32_t *__restrict__ tri_ptr,
-                        const int32_t *__restrict__ tri_col, const int32_t *__restrict__ unit,
-                        const int32_t *__restrict__ pos, const int32_t *__restrict__ step_of,
-                        const int32_t *__restrict__ lev, const int32_t *__restrict__ g_scan,
-                        const int32_t *__restrict__ iptr, uint32_t *key, int32_t *mb) {
+// CROSS dependencies, numbered q = iptr[pos] + r (r-th CROSS dependency of the
+// row in storage order).  Each gets a shared slot of the consumer CTA (after
+// its intra slots).  Delivery: the producer stores into it directly over
+// DSMEM when both CTAs are in one cluster (<= 2 such targets per producer,
+// rt[pos]); otherwise the producer publishes a mailbox (need bit 1) and the
+// consumer CTA's fetcher copies it (an inbound item).  GL: every CROSS
+// dependency polls the mailbox itself (no slot).
+__global__ void k_cross(int n, int nlev, int wpc, int cs, int gl, const int32_t *__restrict__ bperm,
+                        const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
+                        const int32_t *__restrict__ unit, const int32_t *__restrict__ pos,
+                        const int32_t *__restrict__ step_of, const int32_t *__restrict__ lev,
+                        const int32_t *__restrict__ slot_scan, const int32_t *__restrict__ cta_p0,
+                        const int32_t *__restrict__ iptr, int32_t *islot, int32_t *need, int32_t *rtc, int2 *rt,
+                        unsigned char *fetch, uint32_t *ikey, int32_t *iprod) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int i = bperm[p];
-    const int ui = unit[i], si = step_of[p];
+    const int ui = unit[i], si = step_of[p], cc = ui / wpc;
     int q = iptr[p];
-    const uint32_t kk = (uint32_t)(ui / wpc) * (uint32_t)nlev + (uint32_t)lev[i];
+    const int intra = slot_scan[cta_p0[cc + 1]] - slot_scan[cta_p0[cc]];
+    const int q0 = iptr[cta_p0[cc]];
     for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k) {
         const int j = tri_col[k];
-        const int uj = unit[j], pj = pos[j];
-        if (dep_shfl(ui, si, uj, step_of[pj]) || uj / wpc == ui / wpc) continue;   // (no noslot CTA here)
-        key[q] = kk;
-        mb[q] = g_scan[pj];
+        const int uj = unit[j], pj = pos[j], pc = uj / wpc;
+        if (dep_shfl(ui, si, uj, step_of[pj]) || pc == cc) continue;    // (no noslot CTA outside GL)
+        const int slot = kZeroSlots + intra + (q - q0);
+        islot[q] = slot;
+        bool f = true;
+        if (!gl && cs > 1 && pc / cs == cc / cs) {
+            const int r = atomicAdd(&rtc[pj], 1);
+            if (r < 2) {
+                const int code = ((cc % cs) << 24) | slot;
+                if (r == 0) rt[pj].x = code;
+                else rt[pj].y = code;
+                f = false;
+            }
+        }
+        if (f) atomicOr(&need[pj], 2);
+        fetch[q] = f && !gl;
+        ikey[q] = (uint32_t)cc * (uint32_t)nlev + (uint32_t)lev[i];
+        iprod[q] = pj;
         ++q;
     }
 }
 
-__global__ void k_cta_iptr(int K, const int32_t *cta_p0, const int32_t *iptr, int32_t *fptr) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c <= K) fptr[c] = iptr[cta_p0[c]];
+// GL fallback with noslot CTAs: their intra-CTA dependencies use mailboxes too
+__global__ void k_need_gl(int n, int wpc, const int32_t *__restrict__ tri_ptr, const int32_t *__restrict__ tri_col,
+                          const int32_t *__restrict__ unit, const int32_t *__restrict__ pos,
+                          const int32_t *__restrict__ step_of, const unsigned char *__restrict__ noslot, int32_t *need) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int ui = unit[i], pi = pos[i], si = step_of[pi];
+    const bool ns = noslot[ui / wpc] != 0;
+    for (int k = tri_ptr[i]; k < tri_ptr[i + 1]; ++k) {
+        const int j = tri_col[k];
+        const int uj = unit[j], pj = pos[j];
+        if (dep_shfl(ui, si, uj, step_of[pj])) continue;
+        if (uj / wpc != ui / wpc || ns) atomicOr(&need[pj], 2);
+    }
 }
 
-// sorted item q -> fetcher entry {mailbox, slot}; slot of every item (after the CTA's intra slots)
-__global__ void k_item_place(int nitems, int K, int nlev, const uint32_t *iskey, const int32_t *iperm,
-                             const int32_t *imb, const int32_t *slot_scan, const int32_t *cta_p0,
-                             const int32_t *fptr, int2 *fitems, int32_t *islot) {
+__global__ void k_flag_i32(int nq, const unsigned char *f, int32_t *out) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= nitems) return;
-    const int c = (int)(iskey[q] / (uint32_t)nlev);
-    const int intra = slot_scan[cta_p0[c + 1]] - slot_scan[cta_p0[c]];
-    const int slot = intra + (q - fptr[c]);
-    const int item = iperm[q];
-    fitems[q] = make_int2(imb[item], slot);
-    islot[item] = slot;
+    if (q < nq) out[q] = f[q];
+    if (q == nq) out[q] = 0;
+}
+
+// compact the fetched CROSS dependencies into items (key, mailbox, slot)
+__global__ void k_item_compact(int nq, const unsigned char *fetch, const int32_t *fscan, const uint32_t *ikey,
+                               const int32_t *iprod, const int32_t *islot, const int32_t *g_scan, uint32_t *key,
+                               int2 *item) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nq || !fetch[q]) return;
+    const int o = fscan[q];
+    key[o] = ikey[q];
+    item[o] = make_int2(g_scan[iprod[q]], islot[q]);
+}
+
+__global__ void k_item_gather(int nitems, const int32_t *perm, const int2 *item, int2 *fitems) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < nitems) fitems[o] = item[perm[o]];
+}
+
+// first item of every CTA in the (CTA, level)-sorted item list
+__global__ void k_item_ptr(int nitems, int K, int nlev, const uint32_t *skey, int32_t *fptr) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o > nitems) return;
+    const int c1 = o < nitems ? (int)(skey[o] / (uint32_t)nlev) : K;
+    const int c0 = o > 0 ? (int)(skey[o - 1] / (uint32_t)nlev) : -1;
+    for (int c = c0 + 1; c <= c1; ++c) fptr[c] = o;
 }
 
 __global__ void k_need_bits(int n, const int32_t *need, int bit, int32_t *out) {
@@ -395,7 +444,7 @@ __global__ void k_pad_fill(int64_t nrec, unsigned char *__restrict__ ctl, unsign
     const int s = (int)(t >> 5), lane = (int)(t & 31);
     reinterpret_cast<int4 *>(ctl + (size_t)s * kCtlBytes)[lane] = make_int4(kNoneCode, kNoneCode, kNoneCode, -1);
     const T a[kSH] = {T(0), T(0), T(0)};
-    Coef<T>::put(coef + (size_t)s * Coef<T>::BYTES, lane, a, T(0), make_int2(-1, -1));
+    Coef<T>::put(coef + (size_t)s * Coef<T>::BYTES, lane, a, T(0), make_int4(-1, -1, -1, -1));
 }
 
 // padded step index of every step: warp u's steps start at pstart[u]
@@ -425,6 +474,7 @@ __global__ void k_rec_fill(int nsteps, int wpc, const int2 *__restrict__ steps, 
                            const int32_t *__restrict__ slot_scan, const int32_t *__restrict__ g_scan,
                            const int32_t *__restrict__ cta_p0, const int32_t *__restrict__ ovf_ptr,
                            const int32_t *__restrict__ iptr, const int32_t *__restrict__ islot, int gl,
+                           const int2 *__restrict__ rt,
                            unsigned char *__restrict__ ctl, unsigned char *__restrict__ coef,
                            int32_t *__restrict__ ovf_code, T *__restrict__ ovf_val) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -453,7 +503,7 @@ __global__ void k_rec_fill(int nsteps, int wpc, const int2 *__restrict__ steps, 
         const int uj = unit[j], pj = pos[j];
         int32_t c;
         if (dep_shfl(ui, si, uj, step_of[pj])) c = pj - steps[si - 1].x;                  // SHFL: source lane
-        else if (uj / wpc == cta && !ns) c = mk_code(kKSmem, (unsigned)(slot_scan[pj] - slot_base));
+        else if (uj / wpc == cta && !ns) c = mk_code(kKSmem, (unsigned)(kZeroSlots + slot_scan[pj] - slot_base));
         else if (gl) c = mk_code(kKGlob, (unsigned)g_scan[pj]);
         else c = mk_code(kKSmem, (unsigned)islot[item++]);                                // inbound slot
         if (ovf) {
@@ -471,8 +521,9 @@ __global__ void k_rec_fill(int nsteps, int wpc, const int2 *__restrict__ steps, 
     }
     const int nd = need[p];
     reinterpret_cast<int4 *>(cr)[lane] = make_int4(code[0], code[1], code[2], i);
+    const int2 r2 = rt[p];
     Coef<T>::put(fr, lane, a, unit_diag ? T(1) : invd_row[i],
-                 make_int2((nd & 1) ? slot_scan[p] - slot_base : -1, (nd & 2) ? g_scan[p] : -1));
+                 make_int4((nd & 1) ? kZeroSlots + slot_scan[p] - slot_base : -1, (nd & 2) ? g_scan[p] : -1, r2.x, r2.y));
 }
 
 template <typename T>
@@ -490,12 +541,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 __device__ __forceinline__ double lds_volatile(const double *p) {
     double v;
-    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
+    asm volatile("ld.relaxed.cluster.shared::cta.f64 %0, [%1];" : "=d"(v) : "r"(smem_u32(p)));
     return v;
 }
 __device__ __forceinline__ float lds_volatile(const float *p) {
     float v;
-    asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
+    asm volatile("ld.relaxed.cluster.shared::cta.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)));
     return v;
 }
 // predicated value-as-flag loads (return 0 where !pred)
@@ -513,21 +564,21 @@ __device__ __forceinline__ float ldg_flag_if(const float *p, bool pred) {
 }
 __device__ __forceinline__ double lds_flag_if(const double *p, bool pred) {
     unsigned long long v = 0;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.b64 %0, [%1];\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.cluster.shared::cta.b64 %0, [%1];\n\t}"
                  : "+l"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
     return __longlong_as_double((long long)v);
 }
 __device__ __forceinline__ float lds_flag_if(const float *p, bool pred) {
     unsigned v = 0;
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.b32 %0, [%1];\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.cluster.shared::cta.b32 %0, [%1];\n\t}"
                  : "+r"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
     return __uint_as_float(v);
 }
 __device__ __forceinline__ void sts_flag(double *p, double v) {
-    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v));
+    asm volatile("st.relaxed.cluster.shared::cta.f64 [%0], %1;" ::"r"(smem_u32(p)), "d"(v));
 }
 __device__ __forceinline__ void sts_flag(float *p, float v) {
-    asm volatile("st.volatile.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
+    asm volatile("st.relaxed.cluster.shared::cta.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v));
 }
 __device__ __forceinline__ void stg_flag(double *p, double v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"((unsigned long long)__double_as_longlong(v)));
@@ -553,11 +604,11 @@ __device__ __forceinline__ void ldg_flag_into(float &v, const float *p, bool pre
                  : "+f"(v) : "l"(p), "r"((unsigned)pred));
 }
 __device__ __forceinline__ void lds_flag_into(double &v, const double *p, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.f64 %0, [%1];\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.cluster.shared::cta.f64 %0, [%1];\n\t}"
                  : "+d"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
 }
 __device__ __forceinline__ void lds_flag_into(float &v, const float *p, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.volatile.shared.f32 %0, [%1];\n\t}"
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.relaxed.cluster.shared::cta.f32 %0, [%1];\n\t}"
                  : "+f"(v) : "r"(smem_u32(p)), "r"((unsigned)pred));
 }
 __device__ __forceinline__ unsigned hi_word(double v) { return (unsigned)((unsigned long long)__double_as_longlong(v) >> 32); }
@@ -589,7 +640,7 @@ struct BlockArgs {
     int trace_cap;
     const void *b;
     void *x;
-    int G, nslots;
+    int G, nslots;                // nslots: shared slots per CTA including the kZeroSlots
     unsigned long long timeout_ns;
 };
 
@@ -610,42 +661,57 @@ struct Watch {
     }
 };
 
-__device__ __forceinline__ void prefetch_l2_if(const void *p, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q prefetch.global.L2 [%0];\n\t}" ::"l"(p),
-                 "r"((unsigned)pred));
+// Indexed stores / copies predicated on index >= 0 (address and predicate
+// computed inside: no branch, no separate predicate materialisation)
+__device__ __forceinline__ void st_x(double *base, int k, double v) {         // x(k) = v, cache at L2
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.wide.s32 a, %1, 8, %0;\n\t"
+                 "@q st.global.cg.f64 [a], %2;\n\t}" ::"l"(base), "r"(k), "d"(v));
 }
-// predicated stores (no branch in the step body)
-__device__ __forceinline__ void stx_if(double *p, double v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
-                 "r"((unsigned)pred));
+__device__ __forceinline__ void st_x(float *base, int k, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.wide.s32 a, %1, 4, %0;\n\t"
+                 "@q st.global.cg.f32 [a], %2;\n\t}" ::"l"(base), "r"(k), "f"(v));
 }
-__device__ __forceinline__ void stx_if(float *p, float v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f32 [%0], %1;\n\t}" ::"l"(p), "f"(v),
-                 "r"((unsigned)pred));
+__device__ __forceinline__ void st_mb(double *base, int k, double v) {        // mailbox k (relaxed, gpu scope)
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.wide.s32 a, %1, 8, %0;\n\t"
+                 "@q st.relaxed.gpu.global.f64 [a], %2;\n\t}" ::"l"(base), "r"(k), "d"(v));
 }
-__device__ __forceinline__ void stg_flag_if(double *p, double v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f64 [%0], %1;\n\t}" ::"l"(p),
-                 "d"(v), "r"((unsigned)pred));
+__device__ __forceinline__ void st_mb(float *base, int k, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.wide.s32 a, %1, 4, %0;\n\t"
+                 "@q st.relaxed.gpu.global.f32 [a], %2;\n\t}" ::"l"(base), "r"(k), "f"(v));
 }
-__device__ __forceinline__ void stg_flag_if(float *p, float v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f32 [%0], %1;\n\t}" ::"l"(p),
-                 "f"(v), "r"((unsigned)pred));
+__device__ __forceinline__ void st_slot(uint32_t base, int k, double v) {     // shared slot k (volatile)
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .u32 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.lo.u32 a, %1, 8, %0;\n\t"
+                 "@q st.relaxed.cluster.shared::cta.f64 [a], %2;\n\t}" ::"r"(base), "r"(k), "d"(v));
 }
-__device__ __forceinline__ void sts_flag_if(double *p, double v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.f64 [%0], %1;\n\t}" ::"r"(
-                     smem_u32(p)), "d"(v), "r"((unsigned)pred));
+__device__ __forceinline__ void st_slot(uint32_t base, int k, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .u32 a;\n\tsetp.ge.s32 q, %1, 0;\n\tmad.lo.u32 a, %1, 4, %0;\n\t"
+                 "@q st.relaxed.cluster.shared::cta.f32 [a], %2;\n\t}" ::"r"(base), "r"(k), "f"(v));
 }
-__device__ __forceinline__ void sts_flag_if(float *p, float v, bool pred) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.volatile.shared.f32 [%0], %1;\n\t}" ::"r"(
-                     smem_u32(p)), "f"(v), "r"((unsigned)pred));
+// slot read of a term code: SHFL / NONE codes land in the zero slots; SMEM
+// codes (kind bits shifted out by the scale) in their slot
+__device__ __forceinline__ double ld_code(uint32_t base, int c, double) {
+    double v;
+    asm volatile("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %1, 8, %2;\n\tld.relaxed.cluster.shared::cta.f64 %0, [a];\n\t}"
+                 : "=d"(v) : "r"(c), "r"(base));
+    return v;
 }
-// cp.async with a source size: 0 zero-fills the destination without reading
-__device__ __forceinline__ void cp_async_val_z(double *dst, const double *src, bool full) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(full ? 8 : 0)
+__device__ __forceinline__ float ld_code(uint32_t base, int c, float) {
+    float v;
+    asm volatile("{\n\t.reg .u32 a;\n\tmad.lo.u32 a, %1, 4, %2;\n\tld.relaxed.cluster.shared::cta.f32 %0, [a];\n\t}"
+                 : "=f"(v) : "r"(c), "r"(base));
+    return v;
+}
+// cp.async of b(k) (k < 0: zero-fill, nothing read)
+__device__ __forceinline__ void cp_b(uint32_t dst, const double *base, int k) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\t.reg .u32 z;\n\tsetp.ge.s32 q, %2, 0;\n\t"
+                 "mad.wide.s32 a, %2, 8, %1;\n\tselp.u32 z, 8, 0, q;\n\tcp.async.ca.shared.global [%0], [a], 8, z;\n\t}" ::"r"(
+                     dst), "l"(base), "r"(k)
                  : "memory");
 }
-__device__ __forceinline__ void cp_async_val_z(float *dst, const float *src, bool full) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(full ? 4 : 0)
+__device__ __forceinline__ void cp_b(uint32_t dst, const float *base, int k) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .s64 a;\n\t.reg .u32 z;\n\tsetp.ge.s32 q, %2, 0;\n\t"
+                 "mad.wide.s32 a, %2, 4, %1;\n\tselp.u32 z, 4, 0, q;\n\tcp.async.ca.shared.global [%0], [a], 4, z;\n\t}" ::"r"(
+                     dst), "l"(base), "r"(k)
                  : "memory");
 }
 // TMA bulk copy issued by one lane (predicate), no branch
@@ -664,8 +730,8 @@ __device__ __forceinline__ void l2pf_if(const void *src, uint32_t bytes, bool pr
                  : "memory");
 }
 
-// EXT value of one term: shared slot (SMEM) or, in the GL instance only, the
-// mailbox itself (GLOB, polled directly); 0 for other kinds
+// EXT value of one term in the GL / OVF instances: shared slot (SMEM),
+// mailbox polled directly (GLOB, GL only); 0 for other kinds
 template <typename T, bool GL>
 __device__ __forceinline__ T ext_load(int32_t c, const T *slots, const T *gm) {
     T v = T(0);
@@ -675,16 +741,19 @@ __device__ __forceinline__ T ext_load(int32_t c, const T *slots, const T *gm) {
 }
 
 // Re-poll the EXT values of a step that are still the sentinel (warp-uniform
-// loop; out of line: the common case never gets here).  By value: nothing of
-// the caller's state becomes addressable.
+// loop; out of line: the common case never gets here).  By value / through
+// the kernel parameters: nothing of the caller's state becomes addressable.
 template <typename T> struct E3 { T e0, e1, e2; };
 template <typename T, bool GL>
-__device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const T *slots, const T *gm, unsigned *status,
-                                     unsigned long long tmo, unsigned tag) {
+__device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const BlockArgs *pa, unsigned tag) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int wpc = (blockDim.x >> 5) - 1;
+    const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
+    const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
     Watch wd{0, 0};
     for (;;) {
         const bool p0 = is_sent(e.e0), p1 = is_sent(e.e1), p2 = is_sent(e.e2);
-        if (!__any_sync(0xffffffffu, p0 || p1 || p2) || wd.expired(status, tmo, tag)) break;
+        if (!__any_sync(0xffffffffu, p0 || p1 || p2) || wd.expired(pa->status, pa->timeout_ns, tag)) break;
         if (p0) e.e0 = ext_load<T, GL>(c0, slots, gm);
         if (p1) e.e1 = ext_load<T, GL>(c1, slots, gm);
         if (p2) e.e2 = ext_load<T, GL>(c2, slots, gm);
@@ -695,8 +764,13 @@ __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const T *s
 // overflow row (> kSH terms): warp-uniform walk of the lists of the lanes
 // that have one, in storage order, polling SMEM / GLOB values
 template <typename T>
-__device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const int32_t *oc, const T *ov, const T *slots,
-                                    const T *gm, unsigned *status, unsigned long long tmo, unsigned tag) {
+__device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, unsigned tag) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int wpc = (blockDim.x >> 5) - 1;
+    const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
+    const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
+    const int32_t *oc = pa->ovf_code;
+    const T *ov = static_cast<const T *>(pa->ovf_val);
     for (;;) {
         const int32_t c = o >= 0 ? oc[o] : kOvfEnd;
         const bool live = c != kOvfEnd;
@@ -709,7 +783,7 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const int32_t *oc, co
                 Watch w{0, 0};
                 for (;;) {
                     v = k == kKSmem ? lds_volatile(slots + code_idx(c)) : ld_relaxed_val(elem(gm, c));
-                    if (!is_sent(v) || w.expired(status, tmo, tag)) break;
+                    if (!is_sent(v) || w.expired(pa->status, pa->timeout_ns, tag)) break;
                 }
             }
             acc = fnma(ov[o], v, acc);
@@ -722,38 +796,42 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const int32_t *oc, co
 // The fetcher (last warp of a CTA): copies the CTA's inbound values (written
 // to global mailboxes by other CTAs) into their shared slots, in the order
 // the CTA's steps need them.  Lane l owns items l, l+32, ...; it keeps kFw of
-// them polled at once (relaxed loads) and moves on once all kFw arrived.
+// them polled at once (relaxed loads) and refills each window entry as soon
+// as its value arrived (no head-of-line blocking).
 constexpr int kFw = 4;
+constexpr unsigned kFsleep = 128;      // ns between unproductive poll rounds
 template <typename T>
 __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
                         unsigned long long tmo, unsigned tag) {
     const int lane = threadIdx.x & 31;
     Watch wd{0, 0};
-    for (int m = f0 + lane; __any_sync(0xffffffffu, m < f1); m += 32 * kFw) {
-        int2 d[kFw];
-        unsigned todo = 0;
+    int2 d[kFw];
+    int nxt = f0 + lane;                      // next item of this lane
 #pragma unroll
-        for (int k = 0; k < kFw; ++k) {
-            const int i = m + 32 * k;
-            d[k] = i < f1 ? items[i] : make_int2(0, 0);
-            if (i < f1) todo |= 1u << k;
-        }
-        while (__any_sync(0xffffffffu, todo != 0)) {
-            T v[kFw];
+    for (int k = 0; k < kFw; ++k) {
+        d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
+        nxt += 32;
+    }
+    for (;;) {
+        bool live = false;
 #pragma unroll
-            for (int k = 0; k < kFw; ++k) v[k] = (todo >> k) & 1u ? ld_relaxed_val(gm + d[k].x) : T(0);
-            bool got = false;
+        for (int k = 0; k < kFw; ++k) live |= d[k].x >= 0;
+        if (!__any_sync(0xffffffffu, live)) break;
+        T v[kFw];
 #pragma unroll
-            for (int k = 0; k < kFw; ++k)
-                if (((todo >> k) & 1u) && !is_sent(v[k])) {
-                    sts_flag_if(slots + d[k].y, v[k], true);
-                    todo &= ~(1u << k);
-                    got = true;
-                }
-            if (!__any_sync(0xffffffffu, got)) {
-                __nanosleep(64);
-                if (wd.expired(status, tmo, tag)) return;
+        for (int k = 0; k < kFw; ++k) v[k] = d[k].x >= 0 ? ld_relaxed_val(gm + d[k].x) : T(0);
+        bool got = false;
+#pragma unroll
+        for (int k = 0; k < kFw; ++k)
+            if (d[k].x >= 0 && !is_sent(v[k])) {
+                st_slot(smem_u32(slots), d[k].y, v[k]);
+                d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
+                nxt += 32;
+                got = true;
             }
+        if (!__any_sync(0xffffffffu, got)) {      // nothing arrived: back off (polls load L2 for everyone)
+            __nanosleep(kFsleep);
+            if (wd.expired(status, tmo, tag)) return;
         }
     }
 }
@@ -762,17 +840,36 @@ __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots
 template <typename T>
 struct Stage {
     int4 c;          // term codes, row
-    int2 pub;        // shared slot, mailbox
+    int4 pub;        // shared slot, mailbox, remote targets
     Coef<T> f;
 };
+
+// DSMEM store into shared slot (r & 0xFFFFFF) of cluster rank r >> 24 (r >= 0)
+__device__ __forceinline__ void st_remote(uint32_t slots, int r, double v) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .u32 a, ra, rk;\n\tsetp.ge.s32 q, %1, 0;\n\t"
+                 "and.b32 a, %1, 0xFFFFFF;\n\tmad.lo.u32 a, a, 8, %0;\n\tshr.u32 rk, %1, 24;\n\t"
+                 "@q mapa.shared::cluster.u32 ra, a, rk;\n\t@q st.relaxed.cluster.shared::cluster.f64 [ra], %2;\n\t}" ::"r"(
+                     slots), "r"(r), "d"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void st_remote(uint32_t slots, int r, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\t.reg .u32 a, ra, rk;\n\tsetp.ge.s32 q, %1, 0;\n\t"
+                 "and.b32 a, %1, 0xFFFFFF;\n\tmad.lo.u32 a, a, 4, %0;\n\tshr.u32 rk, %1, 24;\n\t"
+                 "@q mapa.shared::cluster.u32 ra, a, rk;\n\t@q st.relaxed.cluster.shared::cluster.f32 [ra], %2;\n\t}" ::"r"(
+                     slots), "r"(r), "f"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // OVF: the plan has rows with more than kSH terms (overflow lists).  GL: the
 // plan keeps GLOB terms (mailboxes polled by the consumer itself: shared
 // slots did not fit); otherwise every cross-CTA value reaches its consumer
 // through the CTA's fetcher warp and a shared slot.  The common instance
 // (no OVF, no GL) carries no code for either.
-template <typename T, bool UNIT, bool OVF, bool GL>
-__global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
+template <typename T, bool UNIT, bool OVF, bool GL, bool CL>
+__global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
     constexpr int CB = Coef<T>::BYTES;
@@ -786,17 +883,19 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
     T *bland = reinterpret_cast<T *>(coefring + (size_t)FR * CB);                      // [DG][32]
     uint64_t *cbar = reinterpret_cast<uint64_t *>(bland + DG * 32);                     // [NCB]
     uint64_t *fbar = cbar + NCB;                                                        // [NFB]
-    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)wpc * WS);
+    T *slots = reinterpret_cast<T *>(smem_raw + (size_t)wpc * WS);                     // [nslots]
+    const uint32_t slots_u32 = smem_u32(slots);
     const T *b = static_cast<const T *>(a.b);
     T *x = static_cast<T *>(a.x);
 
-    for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = Sentinel<T>::value();
+    for (int i = threadIdx.x; i < a.nslots; i += blockDim.x) slots[i] = i < kZeroSlots ? T(0) : Sentinel<T>::value();
     if (lane == 0 && w < wpc) {
         for (int i = 0; i < NCB + NFB; ++i) mbar_init(&cbar[i], 1);
         fence_mbar_init();
     }
     if (threadIdx.x == 0) s_epoch = (unsigned)ld_relaxed(reinterpret_cast<const int *>(a.ctr));
-    __syncthreads();
+    if (CL) cluster_sync_all();      // every CTA of the cluster armed its slots before any DSMEM store
+    else __syncthreads();
     const unsigned epoch = s_epoch;
     const unsigned tag = epoch + 1u;
     T *gm = static_cast<T *>(a.gmb) + (size_t)(epoch & 1u) * a.G;
@@ -805,11 +904,9 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
         for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
             go[i] = Sentinel<T>::value();
     }
-    unsigned *status = a.status;
-    const unsigned long long tmo = a.timeout_ns;
 
     if (w == wpc) {
-        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, status, tmo, tag);
+        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, a.status, a.timeout_ns, tag);
     } else {
     const int u = blockIdx.x * wpc + w;
     const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;    // n: a multiple of UNR
@@ -819,6 +916,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
         const unsigned char *gcoef = a.coef + (size_t)s0 * CB;
         unsigned long long *trc = a.trace != nullptr ? a.trace + (size_t)u * a.trace_cap : nullptr;
         const bool l0 = lane == 0;
+        const uint32_t bland_u32 = smem_u32(bland) + lane * (uint32_t)sizeof(T);
         auto issue = [&](int kb) {              // lane 0: TMA of both streams' blocks kb+DC / kb+DF, L2 prefetch
             const int kc = kb + DC, kf = kb + DF, kp = kb + DP;
             tma_if(ctlring + (size_t)(kc % NCB) * UB * kCtlBytes, gctl + (size_t)kc * UB * kCtlBytes,
@@ -831,29 +929,35 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
         auto wait_bar = [&](uint64_t *bar, uint32_t ph) {
             Watch wd{0, 0};
             while (!mbar_try_wait(bar, ph))
-                if (wd.expired(status, tmo, tag)) break;
+                if (wd.expired(a.status, a.timeout_ns, tag)) break;
         };
         auto try_ctl = [&](int kb) { return kb >= nbx || mbar_try_wait(&cbar[kb % NCB], (uint32_t)((kb / NCB) & 1)); };
         auto try_coef = [&](int kb) { return kb >= nbx || mbar_try_wait(&fbar[kb % NFB], (uint32_t)((kb / NFB) & 1)); };
         auto wait_ctl = [&](int kb) { if (kb < nbx) wait_bar(&cbar[kb % NCB], (uint32_t)((kb / NCB) & 1)); };
         auto wait_coef = [&](int kb) { if (kb < nbx) wait_bar(&fbar[kb % NFB], (uint32_t)((kb / NFB) & 1)); };
-        auto ctl_at = [&](int t) -> int4 {
-            return reinterpret_cast<const int4 *>(ctlring + (size_t)(t & (CR - 1)) * kCtlBytes)[lane];
+        auto ctl_at = [&](int t) -> const int4 * {
+            return reinterpret_cast<const int4 *>(ctlring + (size_t)(t & (CR - 1)) * kCtlBytes) + lane;
         };
         auto load_stage = [&](int t, Stage<T> &S) {
-            S.c = ctl_at(t);
+            S.c = *ctl_at(t);
             const unsigned char *fr = coefring + (size_t)(t & (FR - 1)) * CB;
             S.f.load(fr, lane);
-            S.pub = reinterpret_cast<const int2 *>(fr + Coef<T>::PUB)[lane];
+            S.pub = reinterpret_cast<const int4 *>(fr + Coef<T>::PUB)[lane];
         };
         auto load_ext = [&](const Stage<T> &S, E3<T> &E) {
-            E.e0 = ext_load<T, GL>(S.c.x, slots, gm);
-            E.e1 = ext_load<T, GL>(S.c.y, slots, gm);
-            E.e2 = ext_load<T, GL>(S.c.z, slots, gm);
+            if (OVF || GL) {
+                E.e0 = ext_load<T, GL>(S.c.x, slots, gm);
+                E.e1 = ext_load<T, GL>(S.c.y, slots, gm);
+                E.e2 = ext_load<T, GL>(S.c.z, slots, gm);
+            } else {
+                E.e0 = ld_code(slots_u32, S.c.x, T(0));
+                E.e1 = ld_code(slots_u32, S.c.y, T(0));
+                E.e2 = ld_code(slots_u32, S.c.z, T(0));
+            }
         };
-        // cp.async of b(row) of step t (control entry c), one commit group per step
-        auto far_load = [&](int t, int4 c) {
-            cp_async_val_z(bland + (t & (DG - 1)) * 32 + lane, elem(b, c.w), c.w >= 0);
+        // cp.async of b(row) of step t, one commit group per step
+        auto far_load = [&](int t, int row) {
+            cp_b(bland_u32 + (uint32_t)((t & (DG - 1)) * 32 * sizeof(T)), b, row);
             cp_async_commit();
         };
 
@@ -864,15 +968,11 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
                 l2pf_if(gcoef + (size_t)kb * UB * CB, UB * CB, true);
             }
         for (int kb = -DC; kb < 0; ++kb) issue(kb);     // control blocks 0..DC-1, coefficient blocks 0..DF-1
-        for (int kb = 0; kb <= (PB + UB) / UB; ++kb) wait_ctl(kb);
+        for (int kb = 0; kb <= (DG + UB) / UB; ++kb) wait_ctl(kb);
         wait_coef(0);
         __syncwarp();
-        for (int t = 0; t < PB; ++t) {
-            const int r = ctl_at(t).w;
-            prefetch_l2_if(elem(b, r), r >= 0);
-        }
 #pragma unroll 1
-        for (int j = 0; j < DG; ++j) far_load(j, ctl_at(j));
+        for (int j = 0; j < DG; ++j) far_load(j, ctl_at(j)->w);
         Stage<T> S0, S1;
         load_stage(0, S0);
         load_stage(1, S1);
@@ -880,8 +980,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
         load_ext(S0, E0);
         cp_async_wait<DG - 1>();
         T b0 = bland[lane];
-        int4 nx = ctl_at(DG);                   // control entry of the next far step
-        int npr = ctl_at(PB).w;                 // row of the next L2-prefetch step
+        int nrow = ctl_at(DG)->w;               // row of the next far step
         T xprev = T(0);
 
         // ---- main loop: UNR steps per iteration.  A step is one basic block:
@@ -898,7 +997,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
                     const int kb = t / UB;
                     if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();
                     issue(kb);                           // ring slots of block kb-1 (read >= 3 steps ago)
-                    okc = try_ctl(kb + (PB + UB) / UB);  // read from the next step on
+                    okc = try_ctl(kb + (DG + UB) / UB);  // read from the next step on
                     okf = try_coef(kb + 1);
                 }
                 // ---- the chain on this step's values
@@ -910,24 +1009,22 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
                 acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);
                 acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
                 // ---- loads of later steps (independent of the chain)
-                far_load(t + DG, nx);
-                prefetch_l2_if(elem(b, npr), npr >= 0);
+                far_load(t + DG, nrow);
                 cp_async_wait<DG - 1>();
                 const T b1 = bland[((t + 1) & (DG - 1)) * 32 + lane];
                 E3<T> E1;
                 load_ext(S1, E1);
-                const int4 nx1 = ctl_at(t + 1 + DG);
-                const int npr1 = ctl_at(t + 1 + PB).w;
+                const int nrow1 = ctl_at(t + 1 + DG)->w;
                 Stage<T> S2;
                 load_stage(t + 2, S2);
                 // ---- readiness (value-as-flag; non-EXT terms hold 0) and ring waits
                 const unsigned sh = sent_hi<T>();
                 const bool pend = (hi_word(E0.e0) == sh) | (hi_word(E0.e1) == sh) | (hi_word(E0.e2) == sh);
                 if (__any_sync(0xffffffffu, pend || !okc || !okf)) {
-                    if (!okc) wait_ctl(t / UB + (PB + UB) / UB);
+                    if (!okc) wait_ctl(t / UB + (DG + UB) / UB);
                     if (!okf) wait_coef(t / UB + 1);
                     if (__any_sync(0xffffffffu, pend)) {
-                        E0 = repoll<T, GL>(E0, S0.c.x, S0.c.y, S0.c.z, slots, gm, status, tmo, tag);
+                        E0 = repoll<T, GL>(E0, S0.c.x, S0.c.y, S0.c.z, &a, tag);
                         acc = b0;
                         acc = fnma(S0.f.a0, code_shfl(S0.c.x) ? h0 : E0.e0, acc);
                         acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);
@@ -937,20 +1034,22 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
                 if (OVF) {
                     const bool ovf = S0.c.x >= kOvfBase && code_kind(S0.c.x) == kKNone;
                     if (__any_sync(0xffffffffu, ovf))
-                        acc = ovf_terms<T>(acc, ovf ? S0.c.x - kOvfBase : -1, xprev, a.ovf_code,
-                                           static_cast<const T *>(a.ovf_val), slots, gm, status, tmo, tag);
+                        acc = ovf_terms<T>(acc, ovf ? S0.c.x - kOvfBase : -1, xprev, &a, tag);
                 }
                 const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S0.f.invd;   // a product is never the sentinel
-                sts_flag_if(slots + S0.pub.x, xi, S0.pub.x >= 0);
-                stg_flag_if(elem(gm, S0.pub.y), xi, S0.pub.y >= 0);
-                stx_if(elem(x, S0.c.w), xi, S0.c.w >= 0);
+                st_slot(slots_u32, S0.pub.x, xi);
+                st_mb(gm, S0.pub.y, xi);
+                if (CL) {
+                    st_remote(slots_u32, S0.pub.z, xi);
+                    st_remote(slots_u32, S0.pub.w, xi);
+                }
+                st_x(x, S0.c.w, xi);
                 xprev = xi;
                 S0 = S1;
                 S1 = S2;
                 E0 = E1;
                 b0 = b1;
-                nx = nx1;
-                npr = npr1;
+                nrow = nrow1;
             }
         }
         cp_async_wait<0>();
@@ -958,7 +1057,8 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
     }
     }
 
-    __syncthreads();
+    if (CL) cluster_sync_all();      // no CTA leaves while a cluster peer may still store into it
+    else __syncthreads();
     if (threadIdx.x == 0) {      // the last CTA to finish advances the mailbox epoch
         __threadfence();
         if (atomicAdd(&a.ctr[1], 1u) == gridDim.x - 1) {
@@ -969,14 +1069,15 @@ __global__ void __launch_bounds__(160, 1) k_block(const BlockArgs a) {
     }
 }
 
+template <typename T, bool UNIT>
+void *pick_kernel_u(bool ovf, bool gl, bool cl) {
+    if (gl) return ovf ? (void *)k_block<T, UNIT, true, true, false> : (void *)k_block<T, UNIT, false, true, false>;
+    if (cl) return ovf ? (void *)k_block<T, UNIT, true, false, true> : (void *)k_block<T, UNIT, false, false, true>;
+    return ovf ? (void *)k_block<T, UNIT, true, false, false> : (void *)k_block<T, UNIT, false, false, false>;
+}
 template <typename T>
-void *pick_kernel(int diag, bool ovf, bool gl) {
-    if (diag == SPTRSV_UNIT) {
-        if (gl) return ovf ? (void *)k_block<T, true, true, true> : (void *)k_block<T, true, false, true>;
-        return ovf ? (void *)k_block<T, true, true, false> : (void *)k_block<T, true, false, false>;
-    }
-    if (gl) return ovf ? (void *)k_block<T, false, true, true> : (void *)k_block<T, false, false, true>;
-    return ovf ? (void *)k_block<T, false, true, false> : (void *)k_block<T, false, false, false>;
+void *pick_kernel(int diag, bool ovf, bool gl, bool cl) {
+    return diag == SPTRSV_UNIT ? pick_kernel_u<T, true>(ovf, gl, cl) : pick_kernel_u<T, false>(ovf, gl, cl);
 }
 
 // Structured-grid detection: candidates (nx, nx*ny) from the dependency
@@ -1035,6 +1136,34 @@ sptrsv_status_t detect_grid(sptrsv_handle_t h, const int32_t *tri_ptr, const int
             }
         }
     return SPTRSV_SUCCESS;
+}
+
+// K CTAs of `threads` threads and `smem` dynamic shared memory, in clusters
+// of cs: co-resident?  (Checked on the slot-mode instance, the largest.)
+bool clusters_fit(sptrsv_handle_t h, bool f64, int cs, int K, int threads, size_t smem) {
+    void *kn = f64 ? (void *)k_block<double, false, false, false, true> : (void *)k_block<float, false, false, false, true>;
+    if (cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)K);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    (void)h;
+    return (int64_t)nc * cs >= K;
 }
 
 int i32_at(const int32_t *d, int64_t i, cudaStream_t s, sptrsv_status_t &st) {
@@ -1099,6 +1228,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         if ((st = detect_grid(h, tri_ptr, tri_col, tmp, s, gnx, gny)) != SPTRSV_SUCCESS) return st;
     }
     int K = 1, wpc = 4;
+    B.cs = 1;
     B.grid_nx = B.grid_ny = B.tile_w = B.tile_h = 0;
     if (gnx > 0) {
         // warp tile tw x th columns (<= 32: one step per level), CTA = wx x wy
@@ -1130,7 +1260,21 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             K = cxn * cyn;
             wpc = wx * wy;
             if (K > h->num_sms) return SPTRSV_ERR_NOT_SUPPORTED;
-            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, tw, th, wx, wy, cxn, K, h->uplo == SPTRSV_UPPER, unit);
+            // clusters of CTAs (DSMEM hand-offs): the largest csx x csy <= 8 that
+            // tiles the CTA grid and can be co-resident
+            int csx = 1, csy = 1;
+            static const int cshapes[][2] = {{2, 4}, {4, 2}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}};
+            for (auto &c : cshapes) {
+                if (cxn % c[0] || cyn % c[1]) continue;
+                if (!clusters_fit(h, f64, c[0] * c[1], K, 32 * (wpc + 1), budget)) continue;
+                csx = c[0];
+                csy = c[1];
+                break;
+            }
+            B.cs = csx * csy;
+            B.csx = csx;
+            k_part_tiles<<<eg, 256, 0, s>>>(n, gnx, gny, tw, th, wx, wy, cxn, K, h->uplo == SPTRSV_UPPER, csx, csy,
+                                            unit);
             B.grid_nx = gnx;
             B.grid_ny = gny;
             B.tile_w = tw;
@@ -1208,7 +1352,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     // ---- 4. shared-memory budget, dependency classes, inbound items
     const size_t fixed = (size_t)wpc * wsb;
     if (fixed > budget) return SPTRSV_ERR_NOT_SUPPORTED;
-    const int cap = (int)((budget - fixed) / es);
+    const int cap = (int)((budget - fixed) / es) - kZeroSlots;
     unsigned char *noslot = nullptr;
     int32_t *need = nullptr, *bits = nullptr, *slot_scan = nullptr, *g_scan = nullptr, *ccnt = nullptr;
     int32_t *icnt = nullptr, *iptr = nullptr;
@@ -1221,7 +1365,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     if ((st = tmp.alloc_n(&icnt, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = tmp.alloc_n(&iptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(noslot, 0, (size_t)K, s));
-    // intra-CTA slots (need bit 0), mailboxes (bit 1), cross dependencies per position
+    // intra-CTA slots (need bit 0), CROSS dependencies per position
     SPTRSV_CUDA(cudaMemsetAsync(need, 0, sizeof(int32_t) * ((size_t)n + 1), s));
     k_need<<<eg, 256, 0, s>>>(n, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need, icnt);
     k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
@@ -1229,18 +1373,19 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     if ((st = exclusive_scan_i32(icnt, iptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, iptr, ccnt);
     SPTRSV_CUDA(cudaGetLastError());
-    std::vector<int32_t> hcnt(2 * (size_t)K);
+    std::vector<int32_t> hcnt((size_t)K);
     SPTRSV_CUDA(cudaMemcpyAsync(hcnt.data(), ccnt, sizeof(int32_t) * K, cudaMemcpyDeviceToHost, s));
-    SPTRSV_CUDA(cudaStreamSynchronize(s));
-    // every CTA's intra + inbound slots fit: fetcher mode; else GLOB terms
-    // (GL instance), and CTAs whose intra slots do not fit use mailboxes too
+    const int32_t ncross = i32_at(iptr, n, s, st);      // (synchronizes)
+    if (st != SPTRSV_SUCCESS) return st;
+    // every CTA's intra + CROSS slots fit: slot mode; else the GL instance
+    // (CROSS terms poll mailboxes), and CTAs whose intra slots do not fit use
+    // mailboxes for those too
     bool gl = false;
     int max_slots = 0;
     for (int c = 0; c < K; ++c) {
-        gl |= hcnt[c] > cap;        // hcnt: intra + inbound
+        gl |= hcnt[c] > cap;
         max_slots = std::max(max_slots, hcnt[c]);
     }
-    int32_t nitems = 0;
     if (gl) {
         k_cta_slots<<<(K + 255) / 256, 256, 0, s>>>(K, cta_p0, slot_scan, nullptr, ccnt);   // intra only
         SPTRSV_CUDA(cudaMemcpyAsync(hcnt.data(), ccnt, sizeof(int32_t) * K, cudaMemcpyDeviceToHost, s));
@@ -1259,40 +1404,64 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 0, bits);
             if ((st = exclusive_scan_i32(bits, slot_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
         }
-    } else {
-        nitems = i32_at(iptr, n, s, st);
-        if (st != SPTRSV_SUCCESS) return st;
+        k_need_gl<<<eg, 256, 0, s>>>(n, wpc, tri_ptr, tri_col, unit, pos, step_of, noslot, need);
     }
     B.gl = gl;
+    const int cs = gl ? 1 : B.cs;
+    if (gl) B.cs = 1;
+    // CROSS dependencies: slots, DSMEM targets, fetch flags, mailbox bits
+    int32_t *islot = nullptr, *rtc = nullptr, *iprod = nullptr, *fscan = nullptr;
+    int2 *rt = nullptr;
+    unsigned char *fetch = nullptr;
+    uint32_t *ikey = nullptr;
+    const size_t nq = (size_t)std::max(ncross, 1);
+    if ((st = tmp.alloc_n(&islot, nq)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&iprod, nq)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&fscan, nq + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&ikey, nq)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&fetch, nq)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&rtc, (size_t)n)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&rt, (size_t)n)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(rtc, 0, sizeof(int32_t) * (size_t)n, s));
+    SPTRSV_CUDA(cudaMemsetAsync(rt, 0xFF, sizeof(int2) * (size_t)n, s));
+    if (!gl && ncross > 0)
+        k_cross<<<eg, 256, 0, s>>>(n, nlev, wpc, cs, 0, bperm, tri_ptr, tri_col, unit, pos, step_of, h->d_lev,
+                                   slot_scan, cta_p0, iptr, islot, need, rtc, rt, fetch, ikey, iprod);
     k_need_bits<<<(n + 1 + 255) / 256, 256, 0, s>>>(n, need, 1, bits);
     if ((st = exclusive_scan_i32(bits, g_scan, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
     const int32_t G = i32_at(g_scan, n, s, st);
     if (st != SPTRSV_SUCCESS) return st;
     B.G = (G + 3) / 4 * 4;             // mailbox array stride (16-byte aligned arrays)
-    B.nslots = max_slots;
+    B.nslots = kZeroSlots + max_slots;
     if ((st = h->arena.alloc_n(&B.d_cta_g0, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
     k_cta_g0<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, cta_p0, g_scan, B.d_cta_g0);
-    // inbound items {mailbox, slot} sorted by (CTA, level); rank of every item
-    int32_t *irank = nullptr;
+    // inbound items {mailbox, slot} of the fetched CROSS dependencies, sorted by (CTA, level)
+    int32_t nitems = 0;
+    if (!gl && ncross > 0) {
+        int32_t *fl = nullptr;
+        if ((st = tmp.alloc_n(&fl, nq + 1)) != SPTRSV_SUCCESS) return st;
+        k_flag_i32<<<(int)((nq + 1 + 255) / 256), 256, 0, s>>>(ncross, fetch, fl);
+        if ((st = exclusive_scan_i32(fl, fscan, (int64_t)ncross + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+        nitems = i32_at(fscan, ncross, s, st);
+        if (st != SPTRSV_SUCCESS) return st;
+    }
     if ((st = h->arena.alloc_n(&B.d_fptr, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc_n(&B.d_fitems, (size_t)std::max(nitems, 1))) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&irank, (size_t)std::max(nitems, 1))) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(B.d_fptr, 0, sizeof(int32_t) * ((size_t)K + 1), s));
     if (nitems > 0) {
-        uint32_t *ikey = nullptr, *iskey = nullptr;
-        int32_t *imb = nullptr, *iperm = nullptr;
-        if ((st = tmp.alloc_n(&ikey, nitems)) != SPTRSV_SUCCESS) return st;
-        if ((st = tmp.alloc_n(&iskey, nitems)) != SPTRSV_SUCCESS) return st;
-        if ((st = tmp.alloc_n(&imb, nitems)) != SPTRSV_SUCCESS) return st;
-        if ((st = tmp.alloc_n(&iperm, nitems)) != SPTRSV_SUCCESS) return st;
-        k_items<<<eg, 256, 0, s>>>(n, nlev, wpc, bperm, tri_ptr, tri_col, unit, pos, step_of, h->d_lev, g_scan,
-                                   iptr, ikey, imb);
-        if ((st = radix_sort_pairs(ikey, nullptr, iskey, iperm, nitems, (uint32_t)((uint64_t)K * nlev - 1), tmp, s)) !=
+        uint32_t *key = nullptr, *skey = nullptr;
+        int2 *item = nullptr;
+        int32_t *perm = nullptr;
+        if ((st = tmp.alloc_n(&key, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&skey, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&item, nitems)) != SPTRSV_SUCCESS) return st;
+        if ((st = tmp.alloc_n(&perm, nitems)) != SPTRSV_SUCCESS) return st;
+        k_item_compact<<<(ncross + 255) / 256, 256, 0, s>>>(ncross, fetch, fscan, ikey, iprod, islot, g_scan, key, item);
+        if ((st = radix_sort_pairs(key, nullptr, skey, perm, nitems, (uint32_t)((uint64_t)K * nlev - 1), tmp, s)) !=
             SPTRSV_SUCCESS)
             return st;
-        k_cta_iptr<<<(K + 1 + 255) / 256, 256, 0, s>>>(K, cta_p0, iptr, B.d_fptr);
-        k_item_place<<<(nitems + 255) / 256, 256, 0, s>>>(nitems, K, nlev, iskey, iperm, imb, slot_scan, cta_p0,
-                                                           B.d_fptr, B.d_fitems, irank);
+        k_item_gather<<<(nitems + 255) / 256, 256, 0, s>>>(nitems, perm, item, B.d_fitems);
+        k_item_ptr<<<(nitems + 1 + 255) / 256, 256, 0, s>>>(nitems, K, nlev, skey, B.d_fptr);
         SPTRSV_CUDA(cudaGetLastError());
     }
     B.nitems = nitems;
@@ -1326,22 +1495,23 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         k_rec_fill<double><<<pg, 256, 0, s>>>(nsteps, wpc, steps, pmap, bperm, pos, step_of, unit, tri_ptr, tri_col,
                                               (const double *)tri_val, (const double *)h->d_invd_row,
                                               h->diag == SPTRSV_UNIT, noslot, need, slot_scan, g_scan, cta_p0,
-                                              ovf_ptr, iptr, irank, (int)gl, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
+                                              ovf_ptr, iptr, islot, (int)gl, rt, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
                                               (double *)B.d_ovf_val);
         k_fill_sentinel<double><<<fg, 256, 0, s>>>((double *)B.d_gmb, 2 * (int64_t)std::max(B.G, 4));
     } else {
         k_rec_fill<float><<<pg, 256, 0, s>>>(nsteps, wpc, steps, pmap, bperm, pos, step_of, unit, tri_ptr, tri_col,
                                              (const float *)tri_val, (const float *)h->d_invd_row,
                                              h->diag == SPTRSV_UNIT, noslot, need, slot_scan, g_scan, cta_p0,
-                                             ovf_ptr, iptr, irank, (int)gl, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
+                                             ovf_ptr, iptr, islot, (int)gl, rt, (unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, B.d_ovf_code,
                                              (float *)B.d_ovf_val);
         k_fill_sentinel<float><<<fg, 256, 0, s>>>((float *)B.d_gmb, 2 * (int64_t)std::max(B.G, 4));
     }
     SPTRSV_CUDA(cudaGetLastError());
 
     // ---- launch configuration: K co-resident CTAs of wpc warps
-    void *kn = f64 ? pick_kernel<double>(h->diag, novf > 0, gl) : pick_kernel<float>(h->diag, novf > 0, gl);
-    const size_t smem = fixed + (size_t)max_slots * es;
+    void *kn = f64 ? pick_kernel<double>(h->diag, novf > 0, gl, B.cs > 1)
+                   : pick_kernel<float>(h->diag, novf > 0, gl, B.cs > 1);
+    const size_t smem = fixed + (size_t)B.nslots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 32 * (wpc + 1), smem));
@@ -1379,7 +1549,25 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     a.nslots = B.nslots;
     a.timeout_ns = h->timeout_ns;
     void *args[] = {(void *)&a};
-    SPTRSV_CUDA(cudaLaunchCooperativeKernel(B.kernel, B.nblocks, B.threads, args, B.smem, s));
+    if (B.cs <= 1) {
+        SPTRSV_CUDA(cudaLaunchCooperativeKernel(B.kernel, B.nblocks, B.threads, args, B.smem, s));
+    } else {
+        // clusters of B.cs CTAs; co-residency of all K CTAs was checked at
+        // build time (cudaOccupancyMaxActiveClusters)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)B.nblocks);
+        cfg.blockDim = dim3((unsigned)B.threads);
+        cfg.dynamicSmemBytes = B.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)B.cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SPTRSV_CUDA(cudaLaunchKernelExC(&cfg, B.kernel, args));
+    }
     h->last_block_solve = true;
     return SPTRSV_SUCCESS;
 }

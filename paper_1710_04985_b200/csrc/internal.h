@@ -53,6 +53,7 @@ struct BlockPlan {
     int32_t *d_fptr = nullptr;        // [K+1] inbound item range of every CTA
     int32_t nitems = 0;
     bool gl = false;                  // fallback: consumers poll mailboxes themselves (slots did not fit)
+    int32_t cs = 1, csx = 1;          // CTAs per cluster (DSMEM hand-offs inside a cluster), x extent
     int32_t *d_ovf_code = nullptr;    // overflow lists (rows with > 3 dependencies)
     void *d_ovf_val = nullptr;
     void *d_gmb = nullptr;            // [2][G] mailboxes (value-as-flag), roles swap per solve

@@ -41,9 +41,9 @@ def timed(sv, b, x, reps=20, do_flush=True):
 
 
 def plan(sv):
-    out = (ctypes.c_longlong * 9)()
+    out = (ctypes.c_longlong * 13)()
     lib.sptrsv_dbg_block_plan(ctypes.c_void_p(sv.handle), out)
-    return dict(zip(["K", "wpc", "nsteps", "G", "nslots", "smem", "rec", "tw", "th"], list(out)))
+    return dict(zip(["K", "wpc", "nsteps", "G", "nslots", "smem", "rec", "tw", "th", "cs", "csx", "items", "gl"], list(out)))
 
 
 def run(name, m, uplo="lower", dtype=np.float64, trace=False, check=True):

@@ -13,7 +13,7 @@ lib.sptrsv_dbg_block_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.
 lib.sptrsv_dbg_block_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 m = workloads.stencil((g, g, g), 7, "lower")
 sv = S.from_csr(m, algo="block")
-out = (ctypes.c_longlong * 9)()
+out = (ctypes.c_longlong * 13)()
 lib.sptrsv_dbg_block_plan(ctypes.c_void_p(sv.handle), out)
 K, wpc = out[0], out[1]
 U = K * wpc

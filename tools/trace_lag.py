@@ -11,12 +11,16 @@ ntx, nty = g // tw, g // th
 wx = 2 if wpc >= 2 else 1
 wy = wpc // wx
 cxn = ntx // wx
+cs, csx = (int(d["plan"][9]), int(d["plan"][10])) if len(d["plan"]) > 9 else (1, 1)
+csy = cs // csx
 t0 = tr[tr > 0].min()
 U, cap = tr.shape
 T = {}
 for u in range(U):
     cta, w = divmod(u, wpc)
-    cx, cy = cta % cxn, cta // cxn
+    cl, rk = divmod(cta, cs)
+    ccx, ccy = cl % (cxn // csx), cl // (cxn // csx)
+    cx, cy = ccx * csx + rk % csx, ccy * csy + rk // csx
     tx, ty = cx * wx + w % wx, cy * wy + w // wx
     T[(tx, ty)] = tr[u]
 def at(tx, ty, lev):
@@ -46,6 +50,21 @@ lx = np.array(lags_x); ly = np.array(lags_y)
 for nm, l in (("x", lx), ("y", ly)):
     cross = l[l[:, 1] == 1, 0]; inner = l[l[:, 1] == 0, 0]
     print(f"lag {nm}: CTA crossing median {np.median(cross):.0f} ns (n={len(cross)}), in-CTA median {np.median(inner) if len(inner) else float('nan'):.0f} ns")
+print("cluster", cs, "=", csx, "x", csy)
+# crossings by kind along x / y: warp (in CTA), CTA (in cluster), cluster
+for nm, dx, dy in (("x", 1, 0), ("y", 0, 1)):
+    kinds = {"warp": [], "cta": [], "cluster": []}
+    for (tx, ty) in T:
+        if (tx + dx, ty + dy) not in T: continue
+        lev = tx * tw + ty * th + 64 + (tw if dx else th); lev -= lev % 4
+        a_, b_ = at(tx, ty, lev), at(tx + dx, ty + dy, lev)
+        if np.isnan(a_) or np.isnan(b_): continue
+        c1x, c1y = tx // wx, ty // wy
+        c2x, c2y = (tx + dx) // wx, (ty + dy) // wy
+        if (c1x, c1y) == (c2x, c2y): kinds["warp"].append(b_ - a_)
+        elif (c1x // csx, c1y // csy) == (c2x // csx, c2y // csy): kinds["cta"].append(b_ - a_)
+        else: kinds["cluster"].append(b_ - a_)
+    print(nm, {k: (f"{np.median(v):.0f} ns", len(v)) for k, v in kinds.items() if v})
 # step rate per warp (ns per step) over its middle
 rates = []
 for k, r in T.items():
