@@ -249,6 +249,29 @@ extern "C" int sptrsv_dbg_block_trace(sptrsv_handle_t h, void *dev_buf, int cap)
     return SPTRSV_SUCCESS;
 }
 
+// Inbound-item delivery trace of BLOCK solves: dev_buf holds nitems uint64
+// (%globaltimer when the fetcher stored the item), NULL disables.  Items are
+// reported by sptrsv_dbg_block_items.
+extern "C" int sptrsv_dbg_block_ftrace(sptrsv_handle_t h, void *dev_buf) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->block.ftrace = dev_buf;
+    return SPTRSV_SUCCESS;
+}
+
+// Copies the inbound items {mailbox, slot} (nitems int2, by (CTA, level)), the
+// per-CTA item ranges (K+1 int) and the items' (CTA * nlev + level) keys to host buffers.
+extern "C" int sptrsv_dbg_block_items(sptrsv_handle_t h, void *items, void *fptr, void *keys) {
+    if (!h || !h->block.built) return SPTRSV_ERR_INVALID_VALUE;
+    const sptrsv::BlockPlan &B = h->block;
+    if (keys && B.nitems > 0 && cudaMemcpy(keys, B.d_fkey, sizeof(uint32_t) * B.nitems, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return SPTRSV_ERR_CUDA;
+    if (items && B.nitems > 0 && cudaMemcpy(items, B.d_fitems, sizeof(int2) * B.nitems, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return SPTRSV_ERR_CUDA;
+    if (fptr && cudaMemcpy(fptr, B.d_fptr, sizeof(int32_t) * (B.nblocks + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return SPTRSV_ERR_CUDA;
+    return SPTRSV_SUCCESS;
+}
+
 // BLOCK plan summary for tools: {K, wpc, nsteps, G, nslots, smem, rec_bytes,
 // tile_w, tile_h, cluster size, cluster x extent, inbound items, gl}
 extern "C" int sptrsv_dbg_block_plan(sptrsv_handle_t h, long long *out13) {

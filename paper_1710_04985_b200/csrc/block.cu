@@ -638,6 +638,7 @@ struct BlockArgs {
     unsigned *status;             // [0] epoch + 1 of the last solve that timed out
     unsigned long long *trace;    // debug: per-warp %globaltimer at block starts (NULL: off)
     int trace_cap;
+    unsigned long long *ftrace;   // debug: %globaltimer of every inbound item's delivery (NULL: off)
     const void *b;
     void *x;
     int G, nslots;                // nslots: shared slots per CTA including the kZeroSlots
@@ -802,14 +803,16 @@ constexpr int kFw = 4;
 constexpr unsigned kFsleep = 128;      // ns between unproductive poll rounds
 template <typename T>
 __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
-                        unsigned long long tmo, unsigned tag) {
+                        unsigned long long tmo, unsigned tag, unsigned long long *ftrace) {
     const int lane = threadIdx.x & 31;
     Watch wd{0, 0};
     int2 d[kFw];
+    int id[kFw];
     int nxt = f0 + lane;                      // next item of this lane
 #pragma unroll
     for (int k = 0; k < kFw; ++k) {
         d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
+        id[k] = nxt;
         nxt += 32;
     }
     for (;;) {
@@ -825,7 +828,9 @@ __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots
         for (int k = 0; k < kFw; ++k)
             if (d[k].x >= 0 && !is_sent(v[k])) {
                 st_slot(smem_u32(slots), d[k].y, v[k]);
+                if (ftrace != nullptr) ftrace[id[k]] = gtimer();
                 d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
+                id[k] = nxt;
                 nxt += 32;
                 got = true;
             }
@@ -906,7 +911,8 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
     }
 
     if (w == wpc) {
-        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, a.status, a.timeout_ns, tag);
+        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, a.status, a.timeout_ns, tag,
+                          a.ftrace);
     } else {
     const int u = blockIdx.x * wpc + w;
     const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;    // n: a multiple of UNR
@@ -1461,6 +1467,8 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             SPTRSV_SUCCESS)
             return st;
         k_item_gather<<<(nitems + 255) / 256, 256, 0, s>>>(nitems, perm, item, B.d_fitems);
+        if ((st = h->arena.alloc_n(&B.d_fkey, (size_t)nitems)) != SPTRSV_SUCCESS) return st;   // (tools)
+        SPTRSV_CUDA(cudaMemcpyAsync(B.d_fkey, skey, sizeof(uint32_t) * nitems, cudaMemcpyDeviceToDevice, s));
         k_item_ptr<<<(nitems + 1 + 255) / 256, 256, 0, s>>>(nitems, K, nlev, skey, B.d_fptr);
         SPTRSV_CUDA(cudaGetLastError());
     }
@@ -1543,6 +1551,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     a.status = B.d_ctr + 2;
     a.trace = static_cast<unsigned long long *>(B.trace);
     a.trace_cap = B.trace_cap;
+    a.ftrace = static_cast<unsigned long long *>(B.ftrace);
     a.b = b;
     a.x = x;
     a.G = B.G;

@@ -51,6 +51,7 @@ struct BlockPlan {
     int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
     int2 *d_fitems = nullptr;         // inbound items {mailbox, shared slot} by (CTA, level) (fetcher warps)
     int32_t *d_fptr = nullptr;        // [K+1] inbound item range of every CTA
+    uint32_t *d_fkey = nullptr;       // [nitems] (CTA, level) key of every item (tools)
     int32_t nitems = 0;
     bool gl = false;                  // fallback: consumers poll mailboxes themselves (slots did not fit)
     int32_t cs = 1, csx = 1;          // CTAs per cluster (DSMEM hand-offs inside a cluster), x extent
@@ -60,6 +61,7 @@ struct BlockPlan {
     unsigned *d_ctr = nullptr;        // [0] solve epoch, [1] finished CTAs, [2] timed-out epoch + 1
     int32_t *d_unit = nullptr;        // [n] warp tile of every row (CTA = unit / wpc)
     void *trace = nullptr;            // debug (sptrsv_dbg_block_trace): per-warp step timestamps
+    void *ftrace = nullptr;           // debug: inbound item delivery timestamps
     int32_t trace_cap = 0;
 };
 
