@@ -271,3 +271,66 @@ def test_solve_col_zero_pivot_status():
     m = CSR(2, np.array([0, 1, 2], dtype=np.int32), np.array([0, 0], dtype=np.int32), np.array([1.0, 1.0]))
     with pytest.raises(oracle.OracleError):
         oracle.solve_col(m, np.ones(2))
+
+
+# ---- two-sided pins of the backward-error helper (it was only
+# ever asserted from above).  Reference: the definition evaluated densely in
+# numpy long double, max_i |b - T x|_i / (|T| |x|)_i (Higham, Thm 8.5).
+def _dense_backward_error(m, b, x, uplo, diag):
+    n = m.n
+    T = np.zeros((n, n), dtype=np.longdouble)
+    for i in range(n):
+        for k in range(m.rowptr[i], m.rowptr[i + 1]):
+            j = int(m.colidx[k])
+            if (j < i and uplo == "lower") or (j > i and uplo == "upper"):
+                T[i, j] = m.vals[k]
+            elif j == i and diag == "non_unit":
+                T[i, j] = m.vals[k]
+    if diag == "unit":
+        T[np.arange(n), np.arange(n)] = 1
+    xl = np.asarray(x, dtype=np.longdouble).reshape(n, -1)
+    bl = np.asarray(b, dtype=np.longdouble).reshape(n, -1)
+    res = np.abs(bl - T @ xl)
+    mag = np.abs(T) @ np.abs(xl)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(mag > 0, res / np.where(mag > 0, mag, 1), np.where(res > 0, np.inf, 0))
+    return float(ratio.max())
+
+
+@pytest.mark.parametrize("uplo,diag", [("lower", "non_unit"), ("upper", "non_unit"), ("lower", "unit"),
+                                       ("upper", "unit")])
+def test_backward_error_two_sided(uplo, diag):
+    # integer system: the exact x has backward error exactly 0
+    m = workloads.stencil((9, 7, 5), 7, uplo, diag=8.0)
+    xt = workloads.integer_xtrue(m.n, 1, seed=5)[:, 0]
+    b = oracle.matvec(m, xt, uplo, diag)
+    assert oracle.backward_error(m, b, xt, uplo, diag) == 0.0
+    # one entry perturbed up / down, several entries of mixed sign: equals the
+    # dense long-double definition (a dropped fabs, a dropped term or a
+    # constant return fails one of these)
+    rng = np.random.default_rng(3)
+    for delta_idx, delta in ((m.n // 2, 1e-6), (m.n // 3, -3e-7), (0, 2e-5)):
+        x = xt.astype(np.float64).copy()
+        x[delta_idx] += delta
+        be = oracle.backward_error(m, b, x, uplo, diag)
+        ref = _dense_backward_error(m, b, x, uplo, diag)
+        assert be > 0 and abs(be - ref) <= 1e-12 * ref, (be, ref)
+    x = xt + rng.uniform(-1e-4, 1e-4, size=m.n)
+    be = oracle.backward_error(m, b, x, uplo, diag)
+    ref = _dense_backward_error(m, b, x, uplo, diag)
+    assert abs(be - ref) <= 1e-12 * ref, (be, ref)
+    # multi-column: the max over columns
+    X = np.stack([xt.astype(np.float64), x], axis=1)
+    B = np.stack([b, b], axis=1)
+    assert abs(oracle.backward_error(m, B, X, uplo, diag) - ref) <= 1e-12 * ref
+
+
+def test_backward_error_zero_denominator_and_negative_residual():
+    # x = 0: |T||x| = 0 in every row; row 0 has a zero residual (contributes 0),
+    # row 1 a nonzero one -> infinite backward error
+    m = csr(2, [[0], [0, 1]], vals=[2.0, 1.0, 4.0])
+    assert oracle.backward_error(m, np.array([0.0, 3.0]), np.array([0.0, 0.0])) > 1e300
+    assert oracle.backward_error(m, np.array([0.0, 0.0]), np.array([0.0, 0.0])) == 0.0
+    # a residual of either sign counts by magnitude: b - T x = -0.5 in row 0
+    be = oracle.backward_error(m, np.array([1.5, 1.0]), np.array([1.0, 0.0]))
+    assert abs(be - 0.5 / 2.0) <= 1e-15
