@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "tile", "slfc", "levc", "auto"],
+    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "slfc", "levc", "auto"],
                     help="auto: BLOCK when the analysis detects a structured grid, else SELF")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -94,18 +94,43 @@ def work_counts(m, solves, nrhs, esize):
     return sum(p[0] for p in per), sum(p[1] for p in per)
 
 
-ALGO_NAMES = {0: "self", 1: "level", 2: "block", 4: "tile", 5: "slfc", 6: "levc"}
+ALGO_NAMES = {0: "self", 1: "level", 2: "block", 5: "slfc", 6: "levc"}
 
 
 def kernel_of(info, nrhs):
-    """(dominant kernel, launches per solve) of a handle's solve path."""
+    """(dominant kernel, launches per solve) of a handle's solve path (solve.cu,
+    block.cu, column.cu): SELF and the <= 16-column multi-RHS kernel also launch
+    k_prefill (x := sentinel)."""
     algo = ALGO_NAMES.get(info["algo"], "self")
     if nrhs == 1:
-        return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1), "tile": ("k_tile", 1),
+        return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1),
                 "slfc": ("k_slfc", 1), "levc": ("k_levc", 1)}[algo]
-    if algo in ("block", "tile") and os.environ.get("SPTRSV_MRHS_TILE") == "1":
-        return ("k_tile_mrhs", 1)
-    return ("k_mrhs", 1) if algo in ("self", "slfc") else ("k_level_mrhs", 1)
+    if nrhs <= 16 and algo not in ("level", "levc"):
+        return ("k_mrhs_vf", 2)
+    return ("k_level_mrhs", (nrhs + 127) // 128)
+
+
+def lib_sha256():
+    import hashlib
+    from paper_1710_04985_b200 import build as B
+    try:
+        with open(B.LIB, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()
+    except OSError:
+        return None
+
+
+def host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
 
 
 def measured_peak():
@@ -117,14 +142,20 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(key):
-    """dram read+write bytes per launch from the committed ncu --set full summary."""
+def ncu_traffic(key, sha):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from an ncu --set full capture of THIS library build (entries are
+    keyed by config/kernel/dtype and carry the sha256 of libsptrsv.so they were
+    measured on; any other build -> None)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(key)
+            ent = json.load(f).get(key)
     except Exception:
         return None
+    if not isinstance(ent, dict) or sha is None or ent.get("lib_sha256") != sha:
+        return None
+    return ent.get("bytes")
 
 
 # ------------------------------------------------------------------ clocks
@@ -255,21 +286,83 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(per * 1e3, 4), "higher_is_better": True,
         "scaling": prob["scaling"], "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "gflops": round(flops / per / 1e9, 4),
-        "config": {"workload": config_name(args.config), "n": m.n, "nrhs": int(rhs.shape[1]),
+        "config": {"workload": config_name(args.config, args.dtype), "n": m.n, "nrhs": int(rhs.shape[1]),
                    "bytes_per_step": nbytes, "flops_per_step": flops},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} full oracle solves of {config_name(args.config)}"},
+                         "sample": f"{args.steps} full oracle solves of {config_name(args.config, args.dtype)}",
+                         "host": host_cpu()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_name(cfg):
-    return {1: "cfg1: L+D of 2D 5-point 32x32, fp64, 1 RHS",
-            2: "cfg2: L+D of 3D 7-point 128^3 (n=2097152), fp64, 1 RHS",
-            3: "cfg3: ILU(0) of 3D 27-point 96^3, forward (unit L) + backward (U) solve, fp64",
-            4: "cfg4: generated power-law lower factor n=4194304 nlev=12288, fp64",
-            5: "cfg5: 64 RHS on the 3D 7-point 128^3 factor, column-partitioned over ranks"}[cfg]
+def config_name(cfg, dtype="f64"):
+    p = {"f64": "fp64", "f32": "fp32"}[dtype]
+    return {1: f"cfg1: L+D of 2D 5-point 32x32, {p}, 1 RHS",
+            2: f"cfg2: L+D of 3D 7-point 128^3 (n=2097152), {p}, 1 RHS",
+            3: f"cfg3: ILU(0) of 3D 27-point 96^3, forward (unit L) + backward (U) solve, {p}",
+            4: f"cfg4: generated power-law lower factor n=4194304 nlev=12288, {p}",
+            5: f"cfg5: 64 RHS on the 3D 7-point 128^3 factor, column-partitioned over ranks, {p}"}[cfg]
+
+
+def latency_per_level(S, algo, dt, dev):
+    """Measured time per dependent level of `algo` when nothing but the chain
+    runs: BLOCK on one 8x4-column warp tile of a 7-point grid (one step per
+    level), the row-wise algorithms on a bidiagonal chain (one row per level).
+    nlev x this is the latency floor of a solve."""
+    import torch
+    import workloads
+    if algo == "block":
+        m = workloads.stencil((8, 4, 1024), 7, "lower")
+    else:
+        n = 4096
+        rp = np.arange(0, 2 * n, 2, dtype=np.int32) - 1
+        rp[0] = 0
+        rp = np.append(rp, 2 * n - 1).astype(np.int32)
+        ci = np.empty(2 * n - 1, dtype=np.int32)
+        ci[0] = 0
+        ci[1::2] = np.arange(0, n - 1)
+        ci[2::2] = np.arange(1, n)
+        va = np.empty(2 * n - 1)
+        va[0] = 1.0
+        va[1::2] = -0.5
+        va[2::2] = 1.0
+        m = workloads.CSR(n, rp, ci, va)
+    h = S.from_csr(m, dtype=dt, algo=algo)
+    nlev = h.info()["nlev"]
+    bb = torch.ones(m.n, dtype=dt, device=dev)
+    xx = torch.empty_like(bb)
+    for _ in range(3):
+        h.solve(bb, xx)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        a_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        h.solve(bb, xx)
+        e_.record()
+        e_.synchronize()
+        ts.append(a_.elapsed_time(e_) * 1e-3)
+    return float(np.median(ts)) / nlev, {"probe": f"{'8x4x1024 7-point tile' if algo == 'block' else 'chain n=4096'}",
+                                         "nlev": nlev, "us": round(float(np.median(ts)) * 1e6, 2)}
+
+
+def oracle_parity(m, solves, rhs_np, ours, dtype):
+    """The timed step's output against the CPU oracle on the same input (all
+    columns up to 4; else columns 0, middle, last): max relative error."""
+    import oracle
+    nrhs = rhs_np.shape[1]
+    cols = list(range(nrhs)) if nrhs <= 4 else sorted({0, nrhs // 2, nrhs - 1})
+    z = np.ascontiguousarray(rhs_np[:, cols])
+    npdt = np.float64 if dtype == "f64" else np.float32
+    mm = m.astype(npdt) if npdt is np.float32 else m
+    for uplo, diag in solves:
+        z = oracle.solve(mm, z.astype(npdt), uplo, diag, dtype=npdt)
+    o = ours.reshape(m.n, -1)[:, cols].astype(np.float64)
+    ref = np.asarray(z, dtype=np.float64).reshape(m.n, -1)
+    err = float(np.abs(o - ref).max() / max(np.abs(ref).max(), 1e-300))
+    tol = 1e-10 if dtype == "f64" else 1e-4
+    return {"max_rel_err_vs_oracle": err, "tol": tol, "ok": bool(err <= tol), "columns": cols}
 
 
 # ------------------------------------------------------------------ our arm
@@ -320,7 +413,6 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
 
-    # correctness guard on the timed configuration (sampled; the tests do full parity)
     # events bracket every step and every solve (one kernel each for BLOCK /
     # LEVEL; the per-solve times give the dominant kernel's launch duration)
     nh = len(handles)
@@ -468,6 +560,7 @@ def run_ours(args):
         for h in handles:
             h.set_algo(args.algo)
 
+    out_np = bufs[-1].cpu().numpy() if rank == 0 else None
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -487,9 +580,17 @@ def run_ours(args):
         per, reps = time_oracle(m, solves, rhs_np, args.cpu_budget, min_reps=2)
         cpu = {"value": round(nbytes / per / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                "sample": f"{reps} full oracle solves of the same workload ({per * 1e3:.1f} ms each, "
-                         f"~{args.cpu_budget:.0f} s budget), single-threaded C -O2"}
+                         f"~{args.cpu_budget:.0f} s budget), single-threaded C -O2",
+               "host": host_cpu()}
+    parity = oracle_parity(m, solves, rhs_np, out_np, args.dtype)
+    dom_algo = ALGO_NAMES.get(an_infos[dom]["algo"], "self")
+    try:
+        t_lev, lev_probe = latency_per_level(S, dom_algo if nrhs == 1 else "self", dt, dev)
+    except Exception as e:                 # never fails the bench
+        t_lev, lev_probe = None, {"unavailable": str(e)[:120]}
     eff_algo = "+".join(sorted({ALGO_NAMES.get(i["algo"], "?") for i in an_infos}))
     key = f"cfg{args.config}_{kinfo[dom][0]}_{args.dtype}"
+    sha = lib_sha256()
     clk_s = clk.summary()
     line = {
         "metric": "SpTRSV effective HBM GB/s per solve (fraction of B200 peak)",
@@ -498,7 +599,7 @@ def run_ours(args):
         "higher_is_better": True, "scaling": prob["scaling"], "vs_baseline": None,
         "dtype": args.dtype, "data": "synthetic (seeded generators, workloads/)",
         "gflops": round(total_flops / t_max / 1e9, 3),
-        "config": {"workload": config_name(args.config), "algo": args.algo, "algo_used": eff_algo,
+        "config": {"workload": config_name(args.config, args.dtype), "algo": args.algo, "algo_used": eff_algo,
                    "n": m.n, "nrhs": int(nrhs),
                    "nnz_used": [i["nnz_used"] for i in an_infos], "nlev": [i["nlev"] for i in an_infos],
                    "bytes_per_step": nbytes, "flops_per_step": flops,
@@ -507,12 +608,19 @@ def run_ours(args):
                    "median_us": round(t_med * 1e6, 2), "min_us": round(float(times.min()) * 1e6, 2),
                    "parallelism": f"replicas{world}" if prob["scaling"] == "weak" else f"rhs-partition{world}"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(key), "peak_source": peak_src,
+                     "frac": round(achieved / peak, 4), "traffic": ncu_traffic(key, sha), "peak_source": peak_src,
+                     "traffic_source": "profiles/ncu_traffic.json entry of this libsptrsv.so build (sha256), else null",
                      "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                      "kernel": kinfo[dom][0], "kernel_us": round(t_dom * 1e6, 2),
                      "bytes_per_launch": int(per_solve[dom][0]),
                      "share_of_step": round(t_dom / t_mean, 4),
-                     "latency_floor_note": f"nlev={an_infos[dom]['nlev']} dependent levels per solve"},
+                     "nlev": an_infos[dom]["nlev"],
+                     "ns_per_level_alone": round(t_lev * 1e9, 1) if t_lev else None,
+                     "latency_floor_us": round(an_infos[dom]["nlev"] * t_lev * 1e6, 2) if t_lev else None,
+                     "latency_floor_probe": lev_probe,
+                     "ns_per_level_achieved": round(t_dom * 1e9 / max(1, an_infos[dom]["nlev"]), 1)},
+        "parity": parity,
+        "lib_sha256": sha,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(args.steps * launches_per_step),

@@ -91,7 +91,7 @@ def test_analysis_random_small(S, seed):
     check_analysis(S, m, uplo, "non_unit")
 
 
-def random_triangular_fast(n, avg_deps, seed, uplo, other=0.5):
+def random_triangular_fast(n, avg_deps, seed, uplo, other=0.5, long_frac=0.02):
     """Random triangle with a stored diagonal, some opposite-triangle entries,
     and a few long rows (> 16 deps -> warp-per-row)."""
     rng = np.random.default_rng(seed)
@@ -99,7 +99,7 @@ def random_triangular_fast(n, avg_deps, seed, uplo, other=0.5):
     for i in range(n):
         lo, hi = (0, i) if uplo == "lower" else (i + 1, n)
         span = hi - lo
-        k = min(span, int(rng.poisson(avg_deps)) if rng.random() > 0.02 else int(rng.integers(17, 200)))
+        k = min(span, int(rng.poisson(avg_deps)) if rng.random() > long_frac else int(rng.integers(17, 200)))
         deps = rng.choice(span, size=k, replace=False) + lo if k > 0 else np.zeros(0, dtype=np.int64)
         olo, ohi = (i + 1, n) if uplo == "lower" else (0, i)
         no = min(ohi - olo, int(rng.poisson(other)))
@@ -243,7 +243,8 @@ def test_solve_host_matches(S):
 @pytest.mark.parametrize("nrhs", [2, 3, 33, 64, 100])
 def test_multi_rhs_small(S, nrhs, algo):
     for uplo in ("lower", "upper"):
-        m = random_triangular_fast(3000, 6.0, 5, uplo)
+        m = (random_triangular_fast(3000, 6.0, 5, uplo) if algo != "block"
+             else random_triangular_fast(3000, 1.5, 5, uplo, long_frac=0.004))
         b = workloads.rhs(m.n, nrhs, seed=nrhs)
         x, _ = gpu_solve(S, m, b, uplo=uplo, algo=algo)
         assert relerr(x, oracle.solve(m, b, uplo)) <= 1e-10
@@ -380,7 +381,7 @@ def test_block_grids(S, dims, pts, uplo, dtype):
 def test_block_natural_partition_and_integer(S, seed, uplo, diag):
     """Natural-order partition (no grid): SHFL / SMEM / GLOB / overflow terms
     of every kind; integer-exact grids bitwise, also in place."""
-    m = random_triangular_fast(2500 + 611 * seed, 1.0 + 0.4 * seed, seed, uplo)
+    m = random_triangular_fast(2500 + 611 * seed, 0.8 + 0.25 * seed, seed, uplo, long_frac=0.004)
     assert avg_deps(m, uplo) <= 3
     b = workloads.rhs(m.n, 1, seed=seed)[:, 0]
     ref = oracle.solve(m, b, uplo, diag)
@@ -398,6 +399,51 @@ def test_block_natural_partition_and_integer(S, seed, uplo, diag):
     assert np.array_equal(bt.cpu().numpy(), xt)
 
 
+def random_lower_vec(n, avg_deps, seed, window=None):
+    """Vectorised random lower triangle (diagonally dominant): Poisson(avg)
+    dependencies per row, uniform over [0, i) or over the last `window` rows."""
+    rng = np.random.default_rng(seed)
+    cnt = np.minimum(rng.poisson(avg_deps, size=n), np.arange(n))
+    rows = np.repeat(np.arange(n), cnt)
+    lo = np.zeros(rows.size, dtype=np.int64) if window is None else np.maximum(0, rows - window)
+    cols = lo + (rng.random(rows.size) * (rows - lo)).astype(np.int64)
+    key = np.unique(rows.astype(np.int64) * n + cols)          # sorted, deduplicated (row, col)
+    rows, cols = key // n, key % n
+    allr = np.concatenate([rows, np.arange(n)])
+    allc = np.concatenate([cols, np.arange(n)])
+    o = np.lexsort((allc, allr))
+    allr, allc = allr[o], allc[o]
+    vals = rng.uniform(-1, 1, size=allr.size)
+    diag = allr == allc
+    absum = np.bincount(allr[~diag], weights=np.abs(vals[~diag]), minlength=n)
+    vals[diag] = 1.0 + absum
+    rowptr = np.zeros(n + 1, dtype=np.int32)
+    rowptr[1:] = np.cumsum(np.bincount(allr, minlength=n))
+    return CSR(n, rowptr, allc.astype(np.int32), vals)
+
+
+@pytest.mark.parametrize("n,window", [(60000, 300), (200000, None)])
+def test_block_natural_partition_multi_cta(S, n, window):
+    """Natural partitions over several CTAs: cross-CTA values through mailboxes
+    and fetcher warps (window 300: slots fit), or -- dependencies anywhere
+    below, too many to stage in shared memory -- the GL instance, whose
+    consumers poll the mailboxes themselves."""
+    m = random_lower_vec(n, 2.0, 17, window)
+    b = workloads.rhs(m.n, 1, seed=5)[:, 0]
+    ref = oracle.solve(m, b)
+    x, sv = gpu_solve(S, m, b, algo="block")
+    assert sv.info()["nblocks"] > 1
+    import ctypes
+    lib = ctypes.CDLL(S.LIB_PATH)
+    lib.sptrsv_dbg_block_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    plan = (ctypes.c_longlong * 13)()
+    assert lib.sptrsv_dbg_block_plan(ctypes.c_void_p(sv.handle), plan) == 0
+    assert plan[12] == (1 if window is None else 0)          # GL instance only when slots cannot fit
+    assert relerr(x, ref) <= 1e-10
+    x2, _ = gpu_solve(S, m, b, solver=sv)
+    assert np.array_equal(x, x2)
+
+
 def test_block_refuses_dense_natural_partition(S):
     m, p = workloads.config(4, scale=1 / 64)
     with pytest.raises(S.SptrsvError) as e:
@@ -412,7 +458,7 @@ def test_block_watchdog_timeout_then_clean(S):
     import ctypes
     lib = ctypes.CDLL(S.LIB_PATH)
     lib.sptrsv_dbg_set_timeout_ns.argtypes = [ctypes.c_void_p, ctypes.c_ulonglong]
-    m = chain(200000, sub=-0.5, d=1.0)                   # natural partition: waits on every CTA crossing
+    m = workloads.stencil((64, 64, 48), 7, "lower")     # many warps: downstream ones wait from the start
     b = workloads.rhs(m.n, 1, seed=4)[:, 0]
     sv = S.from_csr(m, algo="block")
     bt = torch.from_numpy(b).cuda()
