@@ -78,19 +78,25 @@ def build_problem(cfg: int, rank: int, world: int):
     return {"m": m, "solves": solves, "rhs": rhs, "scaling": scaling, "params": p}
 
 
-def solve_counts(m, uplo, diag, nrhs, esize):
+def counts_from(n, offd, diag, nrhs, esize):
     """Compulsory bytes and flops of ONE solve (reading Q13):
-    bytes = 4(n+1) + (4+s) nnz(T) + 2 s n nrhs, flops = nrhs (2 #offdiag + n_div)."""
+    bytes = 4(n+1) + (4+s) nnz(T) + 2 s n nrhs, flops = nrhs (2 #offdiag + n_div),
+    nnz(T) = #offdiag + n_div (n_div = n for NON_UNIT, 0 for UNIT)."""
+    ndiv = n if diag == "non_unit" else 0
+    return 4 * (n + 1) + (4 + esize) * (offd + ndiv) + 2 * esize * n * nrhs, nrhs * (2 * offd + ndiv)
+
+
+def handle_counts(infos, solves, n, nrhs, esize):
+    """Per-solve (bytes, flops) from the GPU analysis of each handle (its
+    referenced off-diagonal count, info.nnz_used): the product path never
+    calls the oracle."""
+    return [counts_from(n, i["nnz_used"], diag, nrhs, esize) for i, (_, diag) in zip(infos, solves)]
+
+
+def oracle_counts(m, solves, nrhs, esize):
+    """The same counts for the reference (CPU oracle) arm, from oracle.select."""
     import oracle
-    offd = oracle.select(m, uplo, diag)["nnz_used"]
-    nnz_t = offd + (m.n if diag == "non_unit" else 0)
-    return (4 * (m.n + 1) + (4 + esize) * nnz_t + 2 * esize * m.n * nrhs,
-            nrhs * (2 * offd + (m.n if diag == "non_unit" else 0)))
-
-
-def work_counts(m, solves, nrhs, esize):
-    """Compulsory bytes and flops of one step (all solves of the configuration)."""
-    per = [solve_counts(m, uplo, diag, nrhs, esize) for uplo, diag in solves]
+    per = [counts_from(m.n, oracle.select(m, uplo, diag)["nnz_used"], diag, nrhs, esize) for uplo, diag in solves]
     return sum(p[0] for p in per), sum(p[1] for p in per)
 
 
@@ -271,7 +277,7 @@ def run_reference(args):
     prob = build_problem(args.config, 0, 1)
     m, solves, rhs = prob["m"], prob["solves"], prob["rhs"]
     esize = 8 if args.dtype == "f64" else 4
-    nbytes, flops = work_counts(m, solves, rhs.shape[1], esize)
+    nbytes, flops = oracle_counts(m, solves, rhs.shape[1], esize)
     # warmup W untimed steps, then K timed steps (each = the full solve, bounded by the workload)
     for _ in range(args.warmup):
         time_oracle(m, solves, rhs, 0.0, max_reps=1)
@@ -384,7 +390,6 @@ def run_ours(args):
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     esize = 8 if args.dtype == "f64" else 4
     nrhs = rhs_np.shape[1]
-    nbytes, flops = work_counts(m, solves, nrhs, esize)
 
     stream = torch.cuda.current_stream()
     # warm-up handle: CUDA module loading is not part of the analysis time
@@ -397,6 +402,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     analysis_ms = (time.perf_counter() - t_an) * 1e3
     an_infos = [h.info() for h in handles]
+    per_solve = handle_counts(an_infos, solves, m.n, nrhs, esize)
+    nbytes, flops = sum(p[0] for p in per_solve), sum(p[1] for p in per_solve)
 
     b = torch.from_numpy(np.ascontiguousarray(rhs_np[:, 0] if nrhs == 1 else rhs_np)).to(dev, dt)
     bufs = [torch.empty_like(b) for _ in handles]
@@ -533,7 +540,7 @@ def run_ours(args):
     # extra: the other algorithms on the same problem (context, rank 0 prints)
     extra = {}
     if args.extra and world == 1:
-        for algo in ("self", "level", "block", "tile", "slfc", "levc"):
+        for algo in ("self", "level", "block", "slfc", "levc"):
             if algo == args.algo:
                 continue
             try:
@@ -570,11 +577,12 @@ def run_ours(args):
     # dominant kernel: the solve with the largest mean time; achieved = its
     # algorithmic bytes / its mean launch duration (CUDA events on its stream)
     kinfo = [kernel_of(i, nrhs) for i in an_infos]
-    per_solve = [solve_counts(m, uplo, diag, nrhs, esize) for uplo, diag in solves]
     dom = int(np.argmax(solve_times.mean(axis=0)))
     t_dom = float(solve_times[:, dom].mean())
     achieved = per_solve[dom][0] / t_dom / 1e9
     launches_per_step = sum(k[1] for k in kinfo)
+    # cpu_baseline leg (the one place this arm executes oracle/): the oracle
+    # timed on the host cores, and the timed step's output checked against it
     cpu = None
     if not args.no_cpu and world == 1:
         per, reps = time_oracle(m, solves, rhs_np, args.cpu_budget, min_reps=2)

@@ -258,8 +258,17 @@ extern "C" int sptrsv_dbg_block_ftrace(sptrsv_handle_t h, void *dev_buf) {
     return SPTRSV_SUCCESS;
 }
 
-// Copies the inbound items {mailbox, slot} (nitems int2, by (CTA, level)), the
-// per-CTA item ranges (K+1 int) and the items' (CTA * nlev + level) keys to host buffers.
+// Mailbox publication trace of BLOCK solves (active only while the step
+// trace is on): dev_buf holds G uint64 (%globaltimer when mailbox g was
+// written), NULL disables.
+extern "C" int sptrsv_dbg_block_ptrace(sptrsv_handle_t h, void *dev_buf) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->block.ptrace = dev_buf;
+    return SPTRSV_SUCCESS;
+}
+
+// Copies the inbound items {mailbox, slot} (nitems int2, by (warp, level)), the
+// per-warp item ranges (K*wpc+1 int) and the items' (warp * nlev + level) keys to host buffers.
 extern "C" int sptrsv_dbg_block_items(sptrsv_handle_t h, void *items, void *fptr, void *keys) {
     if (!h || !h->block.built) return SPTRSV_ERR_INVALID_VALUE;
     const sptrsv::BlockPlan &B = h->block;
@@ -267,7 +276,7 @@ extern "C" int sptrsv_dbg_block_items(sptrsv_handle_t h, void *items, void *fptr
         return SPTRSV_ERR_CUDA;
     if (items && B.nitems > 0 && cudaMemcpy(items, B.d_fitems, sizeof(int2) * B.nitems, cudaMemcpyDeviceToHost) != cudaSuccess)
         return SPTRSV_ERR_CUDA;
-    if (fptr && cudaMemcpy(fptr, B.d_fptr, sizeof(int32_t) * (B.nblocks + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+    if (fptr && cudaMemcpy(fptr, B.d_fptr, sizeof(int32_t) * (B.nunits + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
         return SPTRSV_ERR_CUDA;
     return SPTRSV_SUCCESS;
 }

@@ -354,7 +354,7 @@ __global__ void k_cross(int n, int nlev, int wpc, int cs, int gl, const int32_t 
         }
         if (f) atomicOr(&need[pj], 2);
         fetch[q] = f && !gl;
-        ikey[q] = (uint32_t)cc * (uint32_t)nlev + (uint32_t)lev[i];
+        ikey[q] = (uint32_t)ui * (uint32_t)nlev + (uint32_t)lev[i];      // (consumer warp, level)
         iprod[q] = pj;
         ++q;
     }
@@ -398,7 +398,7 @@ __global__ void k_item_gather(int nitems, const int32_t *perm, const int2 *item,
     if (o < nitems) fitems[o] = item[perm[o]];
 }
 
-// first item of every CTA in the (CTA, level)-sorted item list
+// first item of every warp in the (warp, level)-sorted item list
 __global__ void k_item_ptr(int nitems, int K, int nlev, const uint32_t *skey, int32_t *fptr) {
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o > nitems) return;
@@ -639,6 +639,7 @@ struct BlockArgs {
     unsigned long long *trace;    // debug: per-warp %globaltimer at block starts (NULL: off)
     int trace_cap;
     unsigned long long *ftrace;   // debug: %globaltimer of every inbound item's delivery (NULL: off)
+    unsigned long long *ptrace;   // debug: %globaltimer of every mailbox publication, by mailbox (NULL: off)
     const void *b;
     void *x;
     int G, nslots;                // nslots: shared slots per CTA including the kZeroSlots
@@ -748,7 +749,7 @@ template <typename T> struct E3 { T e0, e1, e2; };
 template <typename T, bool GL>
 __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const BlockArgs *pa, unsigned tag) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int wpc = (blockDim.x >> 5) - 1;
+    const int wpc = blockDim.x >> 6;
     const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
     const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
     Watch wd{0, 0};
@@ -767,7 +768,7 @@ __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const Bloc
 template <typename T>
 __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, unsigned tag) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int wpc = (blockDim.x >> 5) - 1;
+    const int wpc = blockDim.x >> 6;
     const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
     const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
     const int32_t *oc = pa->ovf_code;
@@ -799,8 +800,14 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
 // the CTA's steps need them.  Lane l owns items l, l+32, ...; it keeps kFw of
 // them polled at once (relaxed loads) and refills each window entry as soon
 // as its value arrived (no head-of-line blocking).
-constexpr int kFw = 4;
-constexpr unsigned kFsleep = 128;      // ns between unproductive poll rounds
+#ifndef SPTRSV_BLOCK_FW
+#define SPTRSV_BLOCK_FW 4
+#endif
+#ifndef SPTRSV_BLOCK_FSLEEP
+#define SPTRSV_BLOCK_FSLEEP 128
+#endif
+constexpr int kFw = SPTRSV_BLOCK_FW;
+constexpr unsigned kFsleep = SPTRSV_BLOCK_FSLEEP;      // ns between unproductive poll rounds
 template <typename T>
 __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
                         unsigned long long tmo, unsigned tag, unsigned long long *ftrace) {
@@ -835,7 +842,7 @@ __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots
                 got = true;
             }
         if (!__any_sync(0xffffffffu, got)) {      // nothing arrived: back off (polls load L2 for everyone)
-            __nanosleep(kFsleep);
+            if (kFsleep) __nanosleep(kFsleep);
             if (wd.expired(status, tmo, tag)) return;
         }
     }
@@ -874,7 +881,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // through the CTA's fetcher warp and a shared slot.  The common instance
 // (no OVF, no GL) carries no code for either.
 template <typename T, bool UNIT, bool OVF, bool GL, bool CL>
-__global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockArgs a) {
+__global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
     constexpr int CB = Coef<T>::BYTES;
@@ -882,7 +889,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
     static_assert((CR & (CR - 1)) == 0 && (FR & (FR - 1)) == 0, "power-of-two rings");
     constexpr size_t WS = warp_smem_bytes<T>();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int wpc = (blockDim.x >> 5) - 1;            // compute warps; warp wpc is the fetcher
+    const int wpc = blockDim.x >> 6;                  // compute warps 0..wpc-1; warp wpc + g fetches for warp g
     unsigned char *ctlring = smem_raw + (size_t)w * WS;                                // [CR][kCtlBytes]
     unsigned char *coefring = ctlring + (size_t)CR * kCtlBytes;                         // [FR][CB]
     T *bland = reinterpret_cast<T *>(coefring + (size_t)FR * CB);                      // [DG][32]
@@ -910,8 +917,9 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
             go[i] = Sentinel<T>::value();
     }
 
-    if (w == wpc) {
-        if (!GL) fetcher<T>(a.fitems, a.fptr[blockIdx.x], a.fptr[blockIdx.x + 1], gm, slots, a.status, a.timeout_ns, tag,
+    if (w >= wpc) {
+        const int fu = blockIdx.x * wpc + (w - wpc);      // the compute warp whose items this warp fetches
+        if (!GL) fetcher<T>(a.fitems, a.fptr[fu], a.fptr[fu + 1], gm, slots, a.status, a.timeout_ns, tag,
                           a.ftrace);
     } else {
     const int u = blockIdx.x * wpc + w;
@@ -1001,7 +1009,6 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
                 bool okc = true, okf = true;
                 if (j % UB == 0) {          // block start: refill the rings, test the next blocks
                     const int kb = t / UB;
-                    if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();
                     issue(kb);                           // ring slots of block kb-1 (read >= 3 steps ago)
                     okc = try_ctl(kb + (DG + UB) / UB);  // read from the next step on
                     okf = try_coef(kb + 1);
@@ -1037,6 +1044,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
                         acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
                     }
                 }
+                if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();   // step t's inputs present
                 if (OVF) {
                     const bool ovf = S0.c.x >= kOvfBase && code_kind(S0.c.x) == kKNone;
                     if (__any_sync(0xffffffffu, ovf))
@@ -1045,6 +1053,7 @@ __global__ void __launch_bounds__(160, 1) k_block(const __grid_constant__ BlockA
                 const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S0.f.invd;   // a product is never the sentinel
                 st_slot(slots_u32, S0.pub.x, xi);
                 st_mb(gm, S0.pub.y, xi);
+                if (trc != nullptr && a.ptrace != nullptr && S0.pub.y >= 0) a.ptrace[S0.pub.y] = gtimer();
                 if (CL) {
                     st_remote(slots_u32, S0.pub.z, xi);
                     st_remote(slots_u32, S0.pub.w, xi);
@@ -1272,7 +1281,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             static const int cshapes[][2] = {{2, 4}, {4, 2}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}};
             for (auto &c : cshapes) {
                 if (cxn % c[0] || cyn % c[1]) continue;
-                if (!clusters_fit(h, f64, c[0] * c[1], K, 32 * (wpc + 1), budget)) continue;
+                if (!clusters_fit(h, f64, c[0] * c[1], K, 64 * wpc, budget)) continue;
                 csx = c[0];
                 csy = c[1];
                 break;
@@ -1451,9 +1460,9 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         nitems = i32_at(fscan, ncross, s, st);
         if (st != SPTRSV_SUCCESS) return st;
     }
-    if ((st = h->arena.alloc_n(&B.d_fptr, (size_t)K + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = h->arena.alloc_n(&B.d_fitems, (size_t)std::max(nitems, 1))) != SPTRSV_SUCCESS) return st;
-    SPTRSV_CUDA(cudaMemsetAsync(B.d_fptr, 0, sizeof(int32_t) * ((size_t)K + 1), s));
+    if ((st = h->arena.alloc_n(&B.d_fptr, (size_t)U + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = h->arena.alloc_n(&B.d_fitems, (size_t)std::max(nitems, 1) + 2)) != SPTRSV_SUCCESS) return st;   // + L2-prefetch tail padding
+    SPTRSV_CUDA(cudaMemsetAsync(B.d_fptr, 0, sizeof(int32_t) * ((size_t)U + 1), s));
     if (nitems > 0) {
         uint32_t *key = nullptr, *skey = nullptr;
         int2 *item = nullptr;
@@ -1463,13 +1472,13 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
         if ((st = tmp.alloc_n(&item, nitems)) != SPTRSV_SUCCESS) return st;
         if ((st = tmp.alloc_n(&perm, nitems)) != SPTRSV_SUCCESS) return st;
         k_item_compact<<<(ncross + 255) / 256, 256, 0, s>>>(ncross, fetch, fscan, ikey, iprod, islot, g_scan, key, item);
-        if ((st = radix_sort_pairs(key, nullptr, skey, perm, nitems, (uint32_t)((uint64_t)K * nlev - 1), tmp, s)) !=
+        if ((st = radix_sort_pairs(key, nullptr, skey, perm, nitems, (uint32_t)((uint64_t)U * nlev - 1), tmp, s)) !=
             SPTRSV_SUCCESS)
             return st;
         k_item_gather<<<(nitems + 255) / 256, 256, 0, s>>>(nitems, perm, item, B.d_fitems);
         if ((st = h->arena.alloc_n(&B.d_fkey, (size_t)nitems)) != SPTRSV_SUCCESS) return st;   // (tools)
         SPTRSV_CUDA(cudaMemcpyAsync(B.d_fkey, skey, sizeof(uint32_t) * nitems, cudaMemcpyDeviceToDevice, s));
-        k_item_ptr<<<(nitems + 1 + 255) / 256, 256, 0, s>>>(nitems, K, nlev, skey, B.d_fptr);
+        k_item_ptr<<<(nitems + 1 + 255) / 256, 256, 0, s>>>(nitems, U, nlev, skey, B.d_fptr);
         SPTRSV_CUDA(cudaGetLastError());
     }
     B.nitems = nitems;
@@ -1522,11 +1531,11 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     const size_t smem = fixed + (size_t)B.nslots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 32 * (wpc + 1), smem));
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 64 * wpc, smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = 32 * (wpc + 1);          // wpc compute warps + the fetcher
+    B.threads = 64 * wpc;                // wpc compute warps + one fetcher warp each
     B.rec_bytes = kCtlBytes + CB;
     B.nent = (int64_t)npad * (kCtlBytes + CB);
     SPTRSV_CUDA(cudaStreamSynchronize(s));
@@ -1552,6 +1561,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     a.trace = static_cast<unsigned long long *>(B.trace);
     a.trace_cap = B.trace_cap;
     a.ftrace = static_cast<unsigned long long *>(B.ftrace);
+    a.ptrace = static_cast<unsigned long long *>(B.ptrace);
     a.b = b;
     a.x = x;
     a.G = B.G;

@@ -50,7 +50,7 @@ struct BlockPlan {
     void *d_coef = nullptr;           // step records: coefficient stream
     int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
     int2 *d_fitems = nullptr;         // inbound items {mailbox, shared slot} by (CTA, level) (fetcher warps)
-    int32_t *d_fptr = nullptr;        // [K+1] inbound item range of every CTA
+    int32_t *d_fptr = nullptr;        // [K*wpc+1] inbound item range of every compute warp
     uint32_t *d_fkey = nullptr;       // [nitems] (CTA, level) key of every item (tools)
     int32_t nitems = 0;
     bool gl = false;                  // fallback: consumers poll mailboxes themselves (slots did not fit)
@@ -62,6 +62,7 @@ struct BlockPlan {
     int32_t *d_unit = nullptr;        // [n] warp tile of every row (CTA = unit / wpc)
     void *trace = nullptr;            // debug (sptrsv_dbg_block_trace): per-warp step timestamps
     void *ftrace = nullptr;           // debug: inbound item delivery timestamps
+    void *ptrace = nullptr;           // debug: mailbox publication timestamps (with trace on)
     int32_t trace_cap = 0;
 };
 

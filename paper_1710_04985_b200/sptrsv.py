@@ -16,7 +16,8 @@ import numpy as np
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+# SPTRSV_DEV_LIB: a development variant of the library (tools/build_variant.py)
+LIB_PATH = os.environ.get("SPTRSV_DEV_LIB") or _build.LIB
 
 LOWER, UPPER = 0, 1
 NON_UNIT, UNIT = 0, 1

@@ -13,6 +13,7 @@ lib.sptrsv_dbg_block_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.
 lib.sptrsv_dbg_block_plan.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 lib.sptrsv_dbg_block_ftrace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 lib.sptrsv_dbg_block_items.argtypes = [ctypes.c_void_p] * 4
+lib.sptrsv_dbg_block_ptrace.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 m = workloads.stencil((g, g, g), 7, "lower")
 sv = S.from_csr(m, algo="block")
 out = (ctypes.c_longlong * 13)()
@@ -29,16 +30,19 @@ nit = int(out[11])
 fbuf = torch.zeros(max(nit, 1), dtype=torch.int64, device="cuda")
 lib.sptrsv_dbg_block_trace(ctypes.c_void_p(sv.handle), ctypes.c_void_p(buf.data_ptr()), cap)
 lib.sptrsv_dbg_block_ftrace(ctypes.c_void_p(sv.handle), ctypes.c_void_p(fbuf.data_ptr()))
+pbuf = torch.zeros(max(int(out[3]), 1), dtype=torch.int64, device="cuda")
+lib.sptrsv_dbg_block_ptrace(ctypes.c_void_p(sv.handle), ctypes.c_void_p(pbuf.data_ptr()))
 sv.solve(b, x)
 torch.cuda.synchronize()
 lib.sptrsv_dbg_block_trace(ctypes.c_void_p(sv.handle), None, 0)
 lib.sptrsv_dbg_block_ftrace(ctypes.c_void_p(sv.handle), None)
+lib.sptrsv_dbg_block_ptrace(ctypes.c_void_p(sv.handle), None)
 items = np.zeros((max(nit, 1), 2), dtype=np.int32)
-fptr = np.zeros(K + 1, dtype=np.int32)
+fptr = np.zeros(U + 1, dtype=np.int32)
 keys = np.zeros(max(nit, 1), dtype=np.uint32)
 lib.sptrsv_dbg_block_items(ctypes.c_void_p(sv.handle), items.ctypes.data_as(ctypes.c_void_p),
                            fptr.ctypes.data_as(ctypes.c_void_p), keys.ctypes.data_as(ctypes.c_void_p))
 os.makedirs("gpurun_out", exist_ok=True)
 np.savez_compressed(f"gpurun_out/trace_{tag}.npz", tr=buf.view(U, cap).cpu().numpy(), plan=np.array(list(out)), g=g,
-                    ftr=fbuf.cpu().numpy(), items=items, fptr=fptr, keys=keys, nlev=sv.info()["nlev"])
+                    ftr=fbuf.cpu().numpy(), ptr=pbuf.cpu().numpy(), items=items, fptr=fptr, keys=keys, nlev=sv.info()["nlev"])
 print("saved", U, "warps", sv.solve_status())
