@@ -105,14 +105,18 @@ ALGO_NAMES = {0: "self", 1: "level", 2: "block", 5: "slfc", 6: "levc"}
 
 def kernel_of(info, nrhs):
     """(dominant kernel, launches per solve) of a handle's solve path (solve.cu,
-    block.cu, column.cu): SELF and the <= 16-column multi-RHS kernel also launch
-    k_prefill (x := sentinel)."""
+    block.cu, column.cu, mrt.cu -- the selection rules of solve.cu's launch()):
+    SELF and the <= 16-column multi-RHS kernel also launch k_prefill (x :=
+    sentinel)."""
     algo = ALGO_NAMES.get(info["algo"], "self")
     if nrhs == 1:
         return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1),
                 "slfc": ("k_slfc", 1), "levc": ("k_levc", 1)}[algo]
     if nrhs <= 16 and algo not in ("level", "levc"):
         return ("k_mrhs_vf", 2)
+    es = 8 if info["dtype"] == 0 else 4
+    if algo not in ("level", "levc") and info["max_row_deps"] <= 4 and (nrhs * es) % 16 == 0:
+        return ("k_mrt", (nrhs + 63) // 64)          # multi-RHS tile kernel (mrt.cu; aligned torch buffers)
     return ("k_level_mrhs", (nrhs + 127) // 128)
 
 

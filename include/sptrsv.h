@@ -80,8 +80,8 @@ typedef enum {
     SPTRSV_ERR_ALLOC = 4,           /* device or host allocation failed */
     SPTRSV_ERR_CUDA = 5,            /* a CUDA runtime call failed (message via sptrsv_last_cuda_error) */
     SPTRSV_ERR_NOT_SUPPORTED = 6,   /* no sm_100 device, or a size beyond the int32 index space */
-    SPTRSV_ERR_TIMEOUT = 7          /* a BLOCK solve gave up a spin wait (watchdog, default 4 s);
-                                       reported by sptrsv_get_solve_status, x is invalid */
+    SPTRSV_ERR_TIMEOUT = 7          /* a BLOCK or multi-RHS tile solve gave up a spin wait (watchdog,
+                                       default 4 s); reported by sptrsv_get_solve_status, x is invalid */
 } sptrsv_status_t;
 
 typedef struct {
@@ -134,10 +134,14 @@ sptrsv_status_t sptrsv_analyze(int32_t n, const int32_t *rowptr, const int32_t *
  *          x == b (in place, "x is first initialized as f") is allowed;
  *          other overlaps are not.  Caller-owned; valid until the stream
  *          work completes.  Alignment: the dtype's natural alignment.
- *   nrhs   >= 1, any width.  nrhs == 1 uses the handle's algorithm.  nrhs > 1:
- *          nrhs <= 16 (and algorithm not LEVEL / LEVC) the self-scheduled
- *          value-as-flag multi-RHS kernel; otherwise the level-scheduled
- *          multi-RHS kernel over independent column blocks of <= 128.
+ *   nrhs   >= 1, any width.  nrhs == 1 uses the handle's algorithm.  nrhs > 1
+ *          (algorithm not LEVEL / LEVC): nrhs <= 16 the self-scheduled
+ *          value-as-flag multi-RHS kernel; nrhs > 16 on factors with <= 4
+ *          dependencies per row, with b, x 16-byte aligned and nrhs * sizeof
+ *          a multiple of 16 bytes, the multi-RHS tile kernel (column blocks of
+ *          <= 64; its plan is built on the first such solve); otherwise the
+ *          level-scheduled multi-RHS kernel over independent column blocks of
+ *          <= 128 (also for LEVEL / LEVC).
  * Arithmetic per (row, column): s = b(i); s = fma(-a(k), x(ja(k)), s) in CSR
  * storage order; x(i) = s * (1/d(i)) (s for UNIT).  This holds for BLOCK, for
  * every multi-RHS kernel and for SELF / LEVEL rows with <= 16 dependencies,
@@ -147,14 +151,14 @@ sptrsv_status_t sptrsv_analyze(int32_t n, const int32_t *rowptr, const int32_t *
  * shuffle tree and compute b(i) - sum (reproducible, not storage order);
  * SLFC / LEVC accumulate with atomics (order varies run to run).
  * Asynchrony: no host synchronization, except on the first multi-RHS solve of
- * a handle, which builds the per-position CSR (allocates, synchronizes
- * `stream`).  In-place SELF and multi-RHS solves copy b into a handle-owned
+ * a handle (and the first tile-kernel solve), which builds the per-position
+ * CSR or the tile plan (allocates, synchronizes `stream`).  In-place SELF and multi-RHS solves copy b into a handle-owned
  * scratch buffer (stream-ordered allocation, cudaMallocAsync) because x is
  * their flag array.  Run one multi-RHS solve before capturing a CUDA graph.
  * Returns INVALID_VALUE on bad arguments, the analysis status if the handle
  * holds an analysis error, CUDA on a launch failure.  A BLOCK solve whose spin
- * wait exceeded the watchdog returns SUCCESS here (it is asynchronous) and
- * TIMEOUT from sptrsv_get_solve_status.
+ * wait exceeded the watchdog (BLOCK, or the multi-RHS tile kernel) returns
+ * SUCCESS here (it is asynchronous) and TIMEOUT from sptrsv_get_solve_status.
  */
 sptrsv_status_t sptrsv_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs,
                              sptrsv_stream_t stream);
@@ -191,9 +195,10 @@ sptrsv_status_t sptrsv_get_dep_counts(sptrsv_handle_t h, int32_t *dp);
 /*
  * sptrsv_get_solve_status -- synchronizes the device, then reports whether the
  * LAST solve on the handle completed: SUCCESS, or TIMEOUT if it was a BLOCK
- * solve that gave up a spin wait (its x is invalid).  The watchdog is per
- * handle and per solve: the next solve starts clean.  (SPEC.md:259 timeout
- * guard; the other algorithms have no watchdog and always report SUCCESS.)
+ * or multi-RHS tile solve that gave up a spin wait (its x is invalid).  The
+ * watchdog is per handle and per solve: the next solve starts clean.
+ * (SPEC.md:259 timeout guard; the other kernels have no watchdog and always
+ * report SUCCESS.)
  */
 sptrsv_status_t sptrsv_get_solve_status(sptrsv_handle_t h);
 

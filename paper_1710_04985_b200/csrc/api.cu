@@ -209,7 +209,9 @@ extern "C" sptrsv_status_t sptrsv_get_solve_status(sptrsv_handle_t h) {
     if (h->n == 0) return SPTRSV_SUCCESS;
     SPTRSV_CUDA(cudaSetDevice(h->device));
     SPTRSV_CUDA(cudaDeviceSynchronize());
-    return block_solve_status(h);
+    if (h->last_solve == 1) return block_solve_status(h);
+    if (h->last_solve == 2) return mrt_solve_status(h);
+    return SPTRSV_SUCCESS;
 }
 
 extern "C" const char *sptrsv_status_string(sptrsv_status_t s) {
@@ -230,6 +232,25 @@ extern "C" const char *sptrsv_last_cuda_error(void) { return sptrsv::g_last_cuda
 
 // ---------------------------------------------------------------- debug hooks
 // Not part of include/sptrsv.h: test and profiling instrumentation.
+
+// Multi-RHS kernel selection for A/B measurements: 0 automatic, 1 never the
+// tile kernel (value-as-flag / level-scheduled kernels only).
+extern "C" int sptrsv_dbg_mrhs_path(sptrsv_handle_t h, int mode) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->mrhs_path = mode;
+    return SPTRSV_SUCCESS;
+}
+
+// Per-CTA group trace of multi-RHS tile solves: dev_buf holds K x cap x 2
+// uint64 %globaltimer stamps per group (mrt.cu MrtArgs::trace);
+// NULL disables.  Returns the CTA count K in *k_out (plan built by a solve).
+extern "C" int sptrsv_dbg_mrt_trace(sptrsv_handle_t h, void *dev_buf, int cap, int *k_out) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    h->mrt.trace = dev_buf;
+    h->mrt.trace_cap = dev_buf ? cap : 0;
+    if (k_out) *k_out = h->mrt.K;
+    return SPTRSV_SUCCESS;
+}
 
 // BLOCK spin-watchdog timeout of the handle in ns (default 4e9).  Tests set a
 // tiny value to force SPTRSV_ERR_TIMEOUT.

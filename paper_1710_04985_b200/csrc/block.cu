@@ -1191,6 +1191,40 @@ int i32_at(const int32_t *d, int64_t i, cudaStream_t s, sptrsv_status_t &st) {
 
 }  // namespace
 
+// Natural-order CSR (ptr[n+1], col, val) of the referenced strict triangle, in
+// each row's storage order, rebuilt from the chunk layout into `tmp`.
+sptrsv_status_t build_tri_csr(sptrsv_handle_t h, DevArena &tmp, cudaStream_t s, int32_t **ptr_out, int32_t **col_out,
+                              void **val_out) {
+    const int n = h->n;
+    const size_t es = h->esize;
+    sptrsv_status_t st;
+    int32_t *tri_ptr = nullptr, *tri_col = nullptr;
+    void *tri_val = nullptr;
+    const int64_t nnz = h->info.nnz_used;
+    if ((st = tmp.alloc_n(&tri_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&tri_col, (size_t)std::max<int64_t>(nnz, 1))) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc(&tri_val, (size_t)std::max<int64_t>(nnz, 1) * es)) != SPTRSV_SUCCESS) return st;
+    {
+        int32_t *dpx = nullptr;
+        if ((st = tmp.alloc_n(&dpx, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+        SPTRSV_CUDA(cudaMemcpyAsync(dpx, h->d_dp, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+        SPTRSV_CUDA(cudaMemsetAsync(dpx + n, 0, sizeof(int32_t), s));
+        if ((st = exclusive_scan_i32(dpx, tri_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
+    }
+    const int cgrid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
+    if (h->dtype == SPTRSV_F64)
+        k_tri_fill<double><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
+                                                 (const double *)h->d_eval, tri_ptr, tri_col, (double *)tri_val);
+    else
+        k_tri_fill<float><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
+                                                (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
+    SPTRSV_CUDA(cudaGetLastError());
+    *ptr_out = tri_ptr;
+    *col_out = tri_col;
+    *val_out = tri_val;
+    return SPTRSV_SUCCESS;
+}
+
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     BlockPlan &B = h->block;
     const int n = h->n;
@@ -1212,25 +1246,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     // ---- 1. natural-order CSR of the triangle
     int32_t *tri_ptr = nullptr, *tri_col = nullptr;
     void *tri_val = nullptr;
-    const int64_t nnz = h->info.nnz_used;
-    if ((st = tmp.alloc_n(&tri_ptr, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc_n(&tri_col, (size_t)std::max<int64_t>(nnz, 1))) != SPTRSV_SUCCESS) return st;
-    if ((st = tmp.alloc(&tri_val, (size_t)std::max<int64_t>(nnz, 1) * es)) != SPTRSV_SUCCESS) return st;
-    {
-        int32_t *dpx = nullptr;
-        if ((st = tmp.alloc_n(&dpx, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
-        SPTRSV_CUDA(cudaMemcpyAsync(dpx, h->d_dp, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-        SPTRSV_CUDA(cudaMemsetAsync(dpx + n, 0, sizeof(int32_t), s));
-        if ((st = exclusive_scan_i32(dpx, tri_ptr, (int64_t)n + 1, tmp, s)) != SPTRSV_SUCCESS) return st;
-    }
-    const int cgrid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
-    if (f64)
-        k_tri_fill<double><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
-                                                 (const double *)h->d_eval, tri_ptr, tri_col, (double *)tri_val);
-    else
-        k_tri_fill<float><<<cgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_perm, h->d_ecol,
-                                                (const float *)h->d_eval, tri_ptr, tri_col, (float *)tri_val);
-    SPTRSV_CUDA(cudaGetLastError());
+    if ((st = build_tri_csr(h, tmp, s, &tri_ptr, &tri_col, &tri_val)) != SPTRSV_SUCCESS) return st;
 
     const size_t budget = (size_t)max_smem - 1024;          // static smem + slack
 
@@ -1587,7 +1603,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
         cfg.numAttrs = 1;
         SPTRSV_CUDA(cudaLaunchKernelExC(&cfg, B.kernel, args));
     }
-    h->last_block_solve = true;
+    h->last_solve = 1;
     return SPTRSV_SUCCESS;
 }
 
@@ -1595,7 +1611,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
 // word holds the solve's epoch + 1 and the epoch counter has advanced past it.
 sptrsv_status_t block_solve_status(sptrsv_handle_t h) {
     BlockPlan &B = h->block;
-    if (!B.built || !h->last_block_solve) return SPTRSV_SUCCESS;
+    if (!B.built) return SPTRSV_SUCCESS;
     unsigned c[4] = {0, 0, 0, 0};
     SPTRSV_CUDA(cudaMemcpy(c, B.d_ctr, sizeof(c), cudaMemcpyDeviceToHost));
     return (c[2] != 0 && c[2] == c[0]) ? SPTRSV_ERR_TIMEOUT : SPTRSV_SUCCESS;

@@ -66,6 +66,25 @@ struct BlockPlan {
     int32_t trace_cap = 0;
 };
 
+// Multi-RHS tile plan (mrt.cu)
+struct MrtPlan {
+    bool built = false, failed = false;
+    int32_t K = 0, ngroups = 0, nwaits = 0;
+    int32_t *d_gc0 = nullptr;         // [K+1] first group of every CTA
+    int32_t *d_gstart = nullptr;      // [ngroups+1] first solve position of every group
+    int32_t *d_wptr = nullptr;        // [ngroups+1] wait list of every group
+    int2 *d_waits = nullptr;          // {producer CTA, groups needed}
+    int32_t *d_hptr = nullptr;        // [ngroups+1] halo list of every group
+    int32_t *d_hrow = nullptr;        // halo rows (TMA-copied before their group)
+    int32_t nhalo = 0;
+    unsigned char *d_rec = nullptr;   // per-position records
+    unsigned long long *d_prog = nullptr;   // [K] (epoch << 32) | groups done
+    unsigned *d_status = nullptr;     // [0] epoch of the last launch whose wait timed out
+    unsigned epoch = 0, solve_first = 0;
+    void *trace = nullptr;            // debug (sptrsv_dbg_mrt_trace)
+    int32_t trace_cap = 0;
+};
+
 }  // namespace sptrsv
 
 struct sptrsv_handle_s {
@@ -121,9 +140,11 @@ struct sptrsv_handle_s {
     void *d_scratch = nullptr;               // copy of b for in-place value-as-flag solves
     size_t scratch_bytes = 0;
     sptrsv::BlockPlan block;
+    sptrsv::MrtPlan mrt;
+    int mrhs_path = 0;                       // debug (sptrsv_dbg_mrhs_path): 0 auto, 1 never the tile kernel
     // spin watchdog of the BLOCK solve (sptrsv_get_solve_status)
     unsigned long long timeout_ns = 4000000000ull;
-    bool last_block_solve = false;
+    int last_solve = 0;                      // 1: BLOCK, 2: multi-RHS tile (spin-wait kernels with a watchdog)
 };
 
 namespace sptrsv {
@@ -133,6 +154,12 @@ sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nr
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s);
 sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);
 sptrsv_status_t block_solve_status(sptrsv_handle_t h);
+sptrsv_status_t build_tri_csr(sptrsv_handle_t h, DevArena &tmp, cudaStream_t s, int32_t **ptr, int32_t **col,
+                              void **val);                                                   // block.cu
+// multi-RHS tile solve (mrt.cu): plan built on the first eligible multi-RHS solve
+bool mrt_eligible(sptrsv_handle_t h, const void *b, const void *x, int32_t nrhs);
+sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);
+sptrsv_status_t mrt_solve_status(sptrsv_handle_t h);
 sptrsv_status_t column_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);   // column.cu
 sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s);                            // solve.cu
 // device scans (analyze.cu)

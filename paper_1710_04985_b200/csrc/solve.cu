@@ -638,6 +638,17 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
         return SPTRSV_SUCCESS;
     }
     const bool level_req = h->algo == SPTRSV_ALGO_LEVEL || h->algo == SPTRSV_ALGO_LEVC;
+    // multi-RHS with > 16 columns on factors with <= 4 dependencies per row:
+    // the tile kernel (mrt.cu), which streams the matrix once per 64 columns
+    // and keeps each CTA's previous level in shared memory (cfg5, 64 RHS:
+    // 1.69 vs 1.79 ms for the level-scheduled kernel; 32 RHS 1.44-1.49 vs
+    // 1.77 ms; at <= 16 columns the value-as-flag kernel is faster: 1.04 vs
+    // 1.44 ms at 16, 0.59 vs 1.39 ms at 8 -- profiles/mrhs_r2.md).  Falls
+    // through if its plan cannot be built.
+    if (nrhs > kVfMax && !level_req && h->mrhs_path != 1 && mrt_eligible(h, b, x, nrhs)) {
+        sptrsv_status_t st = mrt_solve(h, b, x, nrhs, s);
+        if (st == SPTRSV_SUCCESS || h->mrt.built) return st;
+    }
     // value-as-flag paths (SELF nrhs = 1, multi-RHS up to 16 columns): x is
     // the flag array, so an in-place solve keeps b aside first
     const bool vf = nrhs == 1 || (nrhs <= kVfMax && !level_req);

@@ -608,3 +608,99 @@ def test_levels_kahn_and_syncfree_agree(S, uplo, monkeypatch):
         assert nlev == ref["nlev"]
         assert np.array_equal(lev, ref["lev"]) and np.array_equal(jlev, ref["jlev"])
         assert np.array_equal(ilev, ref["ilev"])
+
+
+# ------------------------------------------------------------ multi-RHS tile kernel (mrt.cu)
+def random_lowdeg(n, seed, uplo, maxdeg=4, window=3000):
+    """Triangle with 0..maxdeg dependencies per row (uniform), at distances
+    1..window (a few per row much farther), diagonally dominant."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [np.arange(n)], [np.arange(n)]
+    deg = rng.integers(0, maxdeg + 1, size=n)
+    for k in range(maxdeg):
+        i = np.nonzero(deg > k)[0]
+        far = rng.random(i.size) < 0.05
+        dist = np.where(far, rng.integers(1, n + 1, size=i.size), rng.integers(1, window + 1, size=i.size))
+        j = i - dist
+        ok = j >= 0
+        rows.append(i[ok])
+        cols.append(j[ok])
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    key = np.unique(r.astype(np.int64) * n + c)
+    r, c = (key // n).astype(np.int64), (key % n).astype(np.int64)
+    if uplo == "upper":
+        r, c = n - 1 - r, n - 1 - c
+        o = np.lexsort((c, r))
+        r, c = r[o], c[o]
+    vals = rng.uniform(-1, 1, size=r.size)
+    diag = r == c
+    absum = np.bincount(r[~diag], weights=np.abs(vals[~diag]), minlength=n)
+    vals[diag] = 1.0 + absum[r[diag]]
+    rowptr = np.zeros(n + 1, dtype=np.int32)
+    rowptr[1:] = np.cumsum(np.bincount(r, minlength=n))
+    return CSR(n, rowptr, c.astype(np.int32), vals)
+
+
+def _mrhs_old_path(S, sv):
+    import ctypes
+    lib = ctypes.CDLL(S.LIB_PATH)
+    lib.sptrsv_dbg_mrhs_path.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    assert lib.sptrsv_dbg_mrhs_path(ctypes.c_void_p(sv.handle), 1) == 0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["7pt_lower", "7pt_upper_unit", "5pt_2d", "natural_lower", "natural_upper"])
+@pytest.mark.parametrize("nrhs", [18, 24, 33, 64, 100])
+def test_mrhs_tile_kernel(S, case, nrhs, dtype):
+    """Multi-RHS tile kernel (factors with <= 4 dependencies per row, grid tile
+    or natural partitions, column blocks of 64): oracle tolerance, bitwise
+    equal to the other multi-RHS kernels (same per-(row, column) arithmetic),
+    run-to-run bitwise, in place, and the solve completes (watchdog quiet)."""
+    algo = "auto"
+    if case == "7pt_lower":
+        m, uplo, diag = workloads.stencil((40, 24, 12), 7, "lower"), "lower", "non_unit"
+    elif case == "7pt_upper_unit":
+        m, uplo, diag = workloads.stencil((24, 40, 10), 7, "upper"), "upper", "unit"
+    elif case == "5pt_2d":
+        m, uplo, diag = workloads.stencil((96, 64), 5, "lower"), "lower", "non_unit"
+    else:
+        uplo = "lower" if case == "natural_lower" else "upper"
+        m, diag, algo = random_lowdeg(30000, 7, uplo), "non_unit", "self"
+    deps = np.diff(m.rowptr) - 1
+    assert deps.max() <= 4
+    B = workloads.rhs(m.n, nrhs, seed=nrhs + 3)
+    ref = oracle.solve(m.astype(dtype), B.astype(dtype), uplo, diag, dtype=dtype)
+    Bt = torch.from_numpy(B.astype(dtype)).cuda()
+    sv = S.from_csr(m, uplo, diag, dtype, algo=algo)
+    X = sv.solve(Bt).cpu().numpy()
+    assert sv.solve_status() == "SUCCESS"
+    assert relerr(X, ref) <= TOL[dtype]
+    assert np.array_equal(X, sv.solve(Bt).cpu().numpy())
+    Bi = Bt.clone()
+    sv.solve(Bi, x=Bi)
+    torch.cuda.synchronize()
+    assert np.array_equal(Bi.cpu().numpy(), X)
+    old = S.from_csr(m, uplo, diag, dtype, algo=algo)
+    _mrhs_old_path(S, old)
+    assert np.array_equal(old.solve(Bt).cpu().numpy(), X)
+
+
+def test_mrhs_tile_kernel_timeout_then_clean(S):
+    """A wait of the tile kernel that exceeds the watchdog is reported as
+    TIMEOUT by sptrsv_get_solve_status; the next solve is clean."""
+    import ctypes
+    m = workloads.stencil((64, 64, 32), 7, "lower")
+    B = torch.from_numpy(workloads.rhs(m.n, 32, seed=1)).cuda()
+    sv = S.from_csr(m, algo="auto")
+    X = sv.solve(B).cpu().numpy()
+    assert sv.solve_status() == "SUCCESS"
+    lib = ctypes.CDLL(S.LIB_PATH)
+    lib.sptrsv_dbg_set_timeout_ns.argtypes = [ctypes.c_void_p, ctypes.c_ulonglong]
+    lib.sptrsv_dbg_set_timeout_ns(ctypes.c_void_p(sv.handle), 1)
+    sv.solve(B)
+    assert sv.solve_status() == "TIMEOUT"
+    lib.sptrsv_dbg_set_timeout_ns(ctypes.c_void_p(sv.handle), 4_000_000_000)
+    X2 = sv.solve(B).cpu().numpy()
+    assert sv.solve_status() == "SUCCESS"
+    assert np.array_equal(X, X2)
