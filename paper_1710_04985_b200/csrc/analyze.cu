@@ -207,7 +207,16 @@ struct AnalysisStatus {
     int32_t max_lev;          // atomicMax (levels kernel)
     unsigned long long ignored;
     unsigned long long used;
+    int32_t max_width;        // atomicMax over levels of ilev[l+1] - ilev[l]
+    int32_t nnz_input;        // rowptr[n]
 };
+
+// summary of the schedule: the widest level (read with the final status)
+__global__ void k_summary(int nlev, const int32_t *ilev, AnalysisStatus *st) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l < nlev) atomicMax(&st->max_width, ilev[l + 1] - ilev[l]);
+}
+__global__ void k_nnz_input(const int32_t *rowptr, int n, AnalysisStatus *st) { st->nnz_input = rowptr[n]; }
 
 __device__ __forceinline__ bool in_tri(int i, int j, int uplo) { return uplo == SPTRSV_LOWER ? (j < i) : (j > i); }
 
@@ -550,22 +559,18 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
                 std::chrono::duration<double, std::milli>(now - tlast).count());
         tlast = now;
     };
-    DevArena tmp;
+    DevArena tmp(s);
     struct Guard {
         DevArena &a;
         ~Guard() { a.release_all(); }
     } guard{tmp};
     sptrsv_status_t st;
 
-    int32_t nnz_host = 0;
-    SPTRSV_CUDA(cudaMemcpyAsync(&nnz_host, rowptr + n, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SPTRSV_CUDA(cudaStreamSynchronize(s));
-    h->info.nnz_input = nnz_host;
-
     AnalysisStatus *d_stat = nullptr;
     if ((st = tmp.alloc_n(&d_stat, 1)) != SPTRSV_SUCCESS) return st;
-    AnalysisStatus init{INT32_MAX, INT32_MAX, 0, -1, 0ull, 0ull};
+    AnalysisStatus init{INT32_MAX, INT32_MAX, 0, -1, 0ull, 0ull, 0, 0};
     SPTRSV_CUDA(cudaMemcpyAsync(d_stat, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    k_nnz_input<<<1, 1, 0, s>>>(rowptr, n, d_stat);
 
     if ((st = h->arena.alloc_n(&h->d_dp, n)) != SPTRSV_SUCCESS) return st;
     if ((st = h->arena.alloc(&h->d_invd_row, (size_t)n * h->esize)) != SPTRSV_SUCCESS) return st;
@@ -580,6 +585,7 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     AnalysisStatus hs;
     SPTRSV_CUDA(cudaMemcpyAsync(&hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s));
     SPTRSV_CUDA(cudaStreamSynchronize(s));
+    h->info.nnz_input = hs.nnz_input;
     h->info.ignored_entries = (int64_t)hs.ignored;
     h->info.nnz_used = (int64_t)hs.used;
     h->info.max_row_deps = hs.max_deps;
@@ -723,13 +729,12 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     h->bar_base = 0;
 
     phase("sync");
-    // summary
-    std::vector<int32_t> il((size_t)nlev + 1);
-    SPTRSV_CUDA(cudaMemcpyAsync(il.data(), h->d_ilev, sizeof(int32_t) * il.size(), cudaMemcpyDeviceToHost, s));
+    // summary: widest level and rowptr[n], one read with the status
+    k_summary<<<(nlev + 255) / 256, 256, 0, s>>>(nlev, h->d_ilev, d_stat);
+    SPTRSV_CUDA(cudaGetLastError());
+    SPTRSV_CUDA(cudaMemcpyAsync(&hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s));
     SPTRSV_CUDA(cudaStreamSynchronize(s));
-    int maxw = 0;
-    for (int l = 0; l < nlev; ++l) maxw = std::max(maxw, il[l + 1] - il[l]);
-    h->info.max_level_width = maxw;
+    h->info.max_level_width = hs.max_width;
     phase("summary");
     return SPTRSV_SUCCESS;
 }

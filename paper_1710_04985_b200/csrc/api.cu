@@ -20,11 +20,12 @@ sptrsv_status_t cuda_fail(cudaError_t e, const char *where) {
 sptrsv_status_t DevArena::alloc(void **p, size_t nbytes) {
     *p = nullptr;
     if (nbytes == 0) nbytes = 16;
-    cudaError_t e = cudaMalloc(p, nbytes);
+    nbytes = (nbytes + 255) & ~(size_t)255;          // 256-byte aligned sub-allocations
+    cudaError_t e = cudaMallocAsync(p, nbytes, stream);
     if (e != cudaSuccess) {
         *p = nullptr;
         cudaGetLastError();
-        return cuda_fail(e, "cudaMalloc");
+        return cuda_fail(e, "cudaMallocAsync");
     }
     ptrs.push_back(*p);
     bytes += (int64_t)nbytes;
@@ -32,9 +33,24 @@ sptrsv_status_t DevArena::alloc(void **p, size_t nbytes) {
 }
 
 void DevArena::release_all() {
-    for (void *p : ptrs) cudaFree(p);
+    for (void *p : ptrs) cudaFreeAsync(p, stream);
     ptrs.clear();
     bytes = 0;
+}
+
+// The default memory pool of the device keeps freed memory for reuse (stream-
+// ordered allocations of later handles and temporaries then cost no driver
+// round trip).
+void keep_pool_memory(int dev) {
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    done[dev] = true;
 }
 
 }  // namespace sptrsv
@@ -77,7 +93,11 @@ extern "C" sptrsv_status_t sptrsv_analyze(int32_t n, const int32_t *rowptr, cons
     h->info.bad_row = -1;
 
     sptrsv_status_t st = SPTRSV_SUCCESS;
+    keep_pool_memory(dev);
+    h->arena.stream = (cudaStream_t)stream;
     if (n > 0) st = analyze_impl(h, rowptr, colidx, vals, (cudaStream_t)stream);
+    if (h->arena.stream != nullptr) SPTRSV_CUDA(cudaStreamSynchronize(h->arena.stream));
+    h->arena.stream = nullptr;               // later builds / frees: the legacy default stream
     h->status = st;
     h->info.status = st;
     h->info.device_bytes = h->arena.bytes;

@@ -1226,10 +1226,11 @@ sptrsv_status_t build_tri_csr(sptrsv_handle_t h, DevArena &tmp, cudaStream_t s, 
 }
 
 sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
+    ArenaStream as_{h->arena, s};     // the handle's allocations in this call: stream-ordered on s
     BlockPlan &B = h->block;
     const int n = h->n;
     const int nlev = h->info.nlev;
-    DevArena tmp;
+    DevArena tmp(s);
     struct Guard {
         DevArena &a;
         ~Guard() { a.release_all(); }

@@ -177,8 +177,9 @@ __global__ void __launch_bounds__(kLevcThreads, 1) k_levc(int nlev, const int32_
 
 template <typename T>
 sptrsv_status_t build_csc(sptrsv_handle_t h, cudaStream_t s) {
+    ArenaStream as_{h->arena, s};     // the handle's allocations in this call: stream-ordered on s
     const int n = h->n;
-    DevArena tmp;
+    DevArena tmp(s);
     struct Guard {
         DevArena &a;
         ~Guard() { a.release_all(); }

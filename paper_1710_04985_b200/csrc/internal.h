@@ -19,15 +19,29 @@ sptrsv_status_t cuda_fail(cudaError_t e, const char *where);
         if (_e != cudaSuccess) return ::sptrsv::cuda_fail(_e, #call);       \
     } while (0)
 
-// Device allocation bookkeeping of one handle.
+// Device allocation bookkeeping of one handle (or of one call's temporaries).
+// Stream-ordered allocations from the device's default memory pool
+// (cudaMallocAsync / cudaFreeAsync on `stream`): no device-wide
+// synchronisation on free, and pool reuse across handles (the pool keeps its
+// memory: release threshold set at the first analysis).
 struct DevArena {
     std::vector<void *> ptrs;
     int64_t bytes = 0;
+    cudaStream_t stream = nullptr;
+    DevArena() = default;
+    explicit DevArena(cudaStream_t s) : stream(s) {}
     sptrsv_status_t alloc(void **p, size_t nbytes);
     template <typename T> sptrsv_status_t alloc_n(T **p, size_t n) {
         return alloc(reinterpret_cast<void **>(p), n * sizeof(T));
     }
     void release_all();
+};
+// Scoped stream of a handle arena's allocations (restored on exit).
+struct ArenaStream {
+    DevArena &a;
+    cudaStream_t old;
+    ArenaStream(DevArena &arena, cudaStream_t s) : a(arena), old(arena.stream) { a.stream = s; }
+    ~ArenaStream() { a.stream = old; }
 };
 
 // Block-schedule (SPTRSV_ALGO_BLOCK) device data; see block.cu.
@@ -148,6 +162,7 @@ struct sptrsv_handle_s {
 };
 
 namespace sptrsv {
+void keep_pool_memory(int dev);
 sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
                              const void *vals, cudaStream_t s);
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);

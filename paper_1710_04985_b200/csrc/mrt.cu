@@ -480,9 +480,10 @@ size_t smem_of(int dtype, int cpl) {
 }
 
 sptrsv_status_t mrt_build(sptrsv_handle_t h, cudaStream_t s) {
+    ArenaStream as_{h->arena, s};     // the handle's allocations in this call: stream-ordered on s
     MrtPlan &M = h->mrt;
     const int n = h->n, nlev = h->info.nlev;
-    DevArena tmp;
+    DevArena tmp(s);
     struct Guard {
         DevArena &a;
         ~Guard() { a.release_all(); }

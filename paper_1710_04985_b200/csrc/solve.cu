@@ -577,8 +577,9 @@ sptrsv_status_t ensure_scratch(sptrsv_handle_t h, size_t bytes, cudaStream_t s) 
 
 template <typename T>
 sptrsv_status_t build_mr(sptrsv_handle_t h, cudaStream_t s) {
+    ArenaStream as_{h->arena, s};     // the handle's allocations in this call: stream-ordered on s
     const int n = h->n;
-    DevArena tmp;
+    DevArena tmp(s);
     struct Guard {
         DevArena &a;
         ~Guard() { a.release_all(); }

@@ -60,3 +60,29 @@ def test_gather_columns_gloo_world2(total):
     expect = [[float(r + 100 * i) for r in range(total)] for i in range(5)]
     for r in range(ws):
         assert out[r] == expect
+
+
+def test_break_even_solves_matches_brute_force():
+    """bench.break_even_solves = Table 7's n_s: the smallest n >= 1
+    with setup_a + n solve_a < setup_b + n solve_b, checked by scanning n."""
+    import importlib.util
+    import os
+    import random
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(os.path.dirname(
+        os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    rng = random.Random(3)
+    for _ in range(400):
+        sa, sb = rng.uniform(0, 0.2), rng.uniform(0, 0.2)
+        ta, tb = rng.uniform(1e-5, 3e-3), rng.uniform(1e-5, 3e-3)
+        got = bench.break_even_solves(sa, ta, sb, tb)
+        want = None
+        for n in range(1, 200000):
+            if sa + n * ta < sb + n * tb:
+                want = n
+                break
+        if want is None:
+            assert got is None or got >= 200000, (sa, ta, sb, tb, got)
+        else:
+            assert got == want, (sa, ta, sb, tb, got, want)
