@@ -424,6 +424,12 @@ def run_ours(args):
     handles = [S.TriangularSolver(m.n, d_rp, d_ci, d_va, uplo, diag, args.algo) for uplo, diag in solves]
     torch.cuda.synchronize()
     analysis_ms = (time.perf_counter() - t_an) * 1e3
+    # numerical refactorization (NEXT-2): new values, same pattern
+    t_up = time.perf_counter()
+    for h in handles:
+        h.update_values(d_rp, d_ci, d_va)
+    torch.cuda.synchronize()
+    update_ms = (time.perf_counter() - t_up) * 1e3
     del d_rp, d_ci, d_va
     an_infos = [h.info() for h in handles]
     per_solve = handle_counts(an_infos, solves, m.n, nrhs, esize)
@@ -637,7 +643,7 @@ def run_ours(args):
                    "n": m.n, "nrhs": int(nrhs),
                    "nnz_used": [i["nnz_used"] for i in an_infos], "nlev": [i["nlev"] for i in an_infos],
                    "bytes_per_step": nbytes, "flops_per_step": flops,
-                   "analysis_ms": round(analysis_ms, 2),
+                   "analysis_ms": round(analysis_ms, 2), "update_values_ms": round(update_ms, 2),
                    "l2": "flushed before every timed solve (256 MiB write)" if flush is not None else "warm",
                    "median_us": round(t_med * 1e6, 2), "min_us": round(float(times.min()) * 1e6, 2),
                    "parallelism": f"replicas{world}" if prob["scaling"] == "weak" else f"rhs-partition{world}"},

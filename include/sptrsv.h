@@ -106,7 +106,8 @@ typedef struct {
  *   n        order of the matrix (n >= 0; n == 0 gives an empty handle).
  *   rowptr   DEVICE pointer, int32[n+1]; colidx DEVICE int32[nnz];
  *   vals     DEVICE pointer to nnz values of `dtype` (may be NULL only if
- *            diag == SPTRSV_UNIT).  Caller-owned; read during the call only.
+ *            diag == SPTRSV_UNIT and the triangle has no off-diagonal entry:
+ *            else INVALID_VALUE).  Caller-owned; read during the call only.
  *   uplo, diag, dtype   as above.
  *   stream   stream for the analysis kernels; the call synchronizes it before
  *            returning, so the inputs may be freed afterwards.
@@ -171,6 +172,23 @@ sptrsv_status_t sptrsv_solve(sptrsv_handle_t h, const void *b, void *x, int32_t 
  */
 sptrsv_status_t sptrsv_solve_host(sptrsv_handle_t h, const void *b_host, void *x_host,
                                   int32_t nrhs, sptrsv_stream_t stream);
+
+/*
+ * sptrsv_update_values -- new values for the analyzed pattern (numerical
+ * refactorization: the ILU factors of matrices with one sparsity
+ * pattern share their triangular patterns, so the setup phase is reused).
+ *   rowptr, colidx, vals   DEVICE pointers: the same CSR pattern as given to
+ *          sptrsv_analyze (identical rowptr / colidx; vals may be NULL only
+ *          for UNIT handles), caller-owned, read during the call only.
+ * Validates with sptrsv_analyze's rules, then replaces the values of every
+ * layout the handle holds (level-ordered rows, BLOCK records, multi-RHS and
+ * column-wise layouts).  Synchronizes `stream` before returning.  Errors:
+ * INVALID_MATRIX / ZERO_PIVOT as sptrsv_analyze; INVALID_VALUE if the
+ * referenced pattern differs from the analyzed one; the handle then keeps
+ * its old values.
+ */
+sptrsv_status_t sptrsv_update_values(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
+                                     const void *vals, sptrsv_stream_t stream);
 
 /* Frees the handle and its device memory.  NULL is a no-op.  Outstanding
  * solves on the handle must have completed. */

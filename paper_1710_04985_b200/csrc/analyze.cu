@@ -537,6 +537,16 @@ __global__ void __launch_bounds__(256) k_fill(int nchunks, const ChunkDesc *__re
         }
     }
 }
+__global__ void k_chunk_eptr(int nchunks, const ChunkDesc *__restrict__ chunks, int64_t *__restrict__ eptr) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nchunks) eptr[c] = chunks[c].eptr;
+}
+// count of positions where two int arrays differ
+__global__ void k_count_diff(int64_t n, const int32_t *__restrict__ a, const int32_t *__restrict__ b, unsigned *cnt) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool d = i < n && a[i] != b[i];
+    if (__any_sync(0xffffffffu, d) && d) atomicAdd(cnt, 1u);
+}
 }  // namespace
 
 static int grid_for(int64_t items, int per_block, int cap) {
@@ -599,6 +609,9 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
         h->info.zero_pivot_row = hs.zero_pivot_row;
         return SPTRSV_ERR_ZERO_PIVOT;
     }
+    // UNIT without values: only a triangle without off-diagonal entries has
+    // nothing to read (it used to solve with zero coefficients)
+    if (!vals && hs.used > 0) return SPTRSV_ERR_INVALID_VALUE;
 
     phase("validate");
     // a3: levels
@@ -736,6 +749,79 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     h->info.max_level_width = hs.max_width;
     phase("summary");
+    return SPTRSV_SUCCESS;
+}
+
+// sptrsv_update_values (NEXT-2; numerical refactorization keeps the
+// pattern, so the analysis is reused): validate the new values with the same
+// rules as sptrsv_analyze, check that the referenced pattern is the analyzed
+// one (dependency counts and the level-ordered column ids equal), then
+// replace the values of every layout the handle holds.  On any error the
+// handle keeps its old values.
+sptrsv_status_t update_values_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
+                                   const void *vals, cudaStream_t s) {
+    const int n = h->n;
+    DevArena tmp(s);
+    struct Guard {
+        DevArena &a;
+        ~Guard() { a.release_all(); }
+    } guard{tmp};
+    sptrsv_status_t st;
+    AnalysisStatus *d_stat = nullptr;
+    int32_t *dp = nullptr, *ecol = nullptr;
+    void *invd_row = nullptr, *eval = nullptr, *invd = nullptr;
+    int64_t *eptr = nullptr;
+    unsigned *cnt = nullptr;
+    const size_t es = h->esize;
+    if ((st = tmp.alloc_n(&d_stat, 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&dp, (size_t)n)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc(&invd_row, (size_t)n * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&ecol, (size_t)std::max<int64_t>(h->nent, 1))) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc(&eval, (size_t)std::max<int64_t>(h->nent, 1) * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc(&invd, (size_t)n * es)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&eptr, (size_t)h->nchunks + 1)) != SPTRSV_SUCCESS) return st;
+    if ((st = tmp.alloc_n(&cnt, 2)) != SPTRSV_SUCCESS) return st;
+    AnalysisStatus init{INT32_MAX, INT32_MAX, 0, -1, 0ull, 0ull, 0, 0};
+    SPTRSV_CUDA(cudaMemcpyAsync(d_stat, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    SPTRSV_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned), s));
+    const int vgrid = grid_for((int64_t)n * 32, 256, h->num_sms * 16);
+    const int fgrid = grid_for((int64_t)h->nchunks * 32, 256, h->num_sms * 16);
+    const bool f64 = h->dtype == SPTRSV_F64;
+    if (f64)
+        k_validate<double><<<vgrid, 256, 0, s>>>(n, rowptr, colidx, (const double *)vals, h->uplo, h->diag, dp,
+                                                 (double *)invd_row, d_stat);
+    else
+        k_validate<float><<<vgrid, 256, 0, s>>>(n, rowptr, colidx, (const float *)vals, h->uplo, h->diag, dp,
+                                                (float *)invd_row, d_stat);
+    k_count_diff<<<(n + 255) / 256, 256, 0, s>>>(n, dp, h->d_dp, cnt);
+    if (h->nchunks > 0) {
+        k_chunk_eptr<<<(h->nchunks + 255) / 256, 256, 0, s>>>(h->nchunks, h->d_chunks, eptr);
+        if (f64)
+            k_fill<double><<<fgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, eptr, h->d_perm, rowptr, colidx,
+                                                 (const double *)vals, (const double *)invd_row, h->uplo, ecol,
+                                                 (double *)eval, (double *)invd);
+        else
+            k_fill<float><<<fgrid, 256, 0, s>>>(h->nchunks, h->d_chunks, eptr, h->d_perm, rowptr, colidx,
+                                                (const float *)vals, (const float *)invd_row, h->uplo, ecol,
+                                                (float *)eval, (float *)invd);
+        k_count_diff<<<(int)((h->nent + 255) / 256), 256, 0, s>>>(h->nent, ecol, h->d_ecol, cnt + 1);
+    }
+    SPTRSV_CUDA(cudaGetLastError());
+    AnalysisStatus hs;
+    unsigned hc[2] = {0, 0};
+    SPTRSV_CUDA(cudaMemcpyAsync(&hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    if (hs.bad_row != INT32_MAX) return SPTRSV_ERR_INVALID_MATRIX;
+    if (hs.zero_pivot_row != INT32_MAX) return SPTRSV_ERR_ZERO_PIVOT;
+    if (hc[0] != 0 || hc[1] != 0 || (int64_t)hs.used != h->info.nnz_used) return SPTRSV_ERR_INVALID_VALUE;   // not the analyzed pattern
+    // commit: level-ordered layout
+    SPTRSV_CUDA(cudaMemcpyAsync(h->d_invd_row, invd_row, (size_t)n * es, cudaMemcpyDeviceToDevice, s));
+    SPTRSV_CUDA(cudaMemcpyAsync(h->d_invd, invd, (size_t)n * es, cudaMemcpyDeviceToDevice, s));
+    if (h->nent > 0) SPTRSV_CUDA(cudaMemcpyAsync(h->d_eval, eval, (size_t)h->nent * es, cudaMemcpyDeviceToDevice, s));
+    // derived layouts
+    if ((st = refresh_derived_values(h, s)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
     return SPTRSV_SUCCESS;
 }
 

@@ -153,6 +153,16 @@ extern "C" sptrsv_status_t sptrsv_solve_host(sptrsv_handle_t h, const void *b_ho
     return SPTRSV_SUCCESS;
 }
 
+extern "C" sptrsv_status_t sptrsv_update_values(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
+                                                 const void *vals, sptrsv_stream_t stream) {
+    if (!h) return SPTRSV_ERR_INVALID_VALUE;
+    if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n == 0) return SPTRSV_SUCCESS;
+    if (!rowptr || !colidx || (!vals && h->diag == SPTRSV_NON_UNIT)) return SPTRSV_ERR_INVALID_VALUE;
+    SPTRSV_CUDA(cudaSetDevice(h->device));
+    return update_values_impl(h, rowptr, colidx, vals, (cudaStream_t)stream);
+}
+
 extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
     if (!h) return SPTRSV_SUCCESS;
     cudaSetDevice(h->device);

@@ -526,6 +526,32 @@ __global__ void k_rec_fill(int nsteps, int wpc, const int2 *__restrict__ steps, 
                  make_int4((nd & 1) ? kZeroSlots + slot_scan[p] - slot_base : -1, (nd & 2) ? g_scan[p] : -1, r2.x, r2.y));
 }
 
+// new values into the records (NEXT-2 value update): every real lane of every
+// step keeps its codes and publication targets; its coefficients (or its
+// overflow list's values) and 1/d are re-read in storage order
+template <typename T>
+__global__ void k_rec_refill(int64_t npad, const unsigned char *__restrict__ ctl, unsigned char *__restrict__ coef,
+                             const int32_t *__restrict__ tri_ptr, const T *__restrict__ tri_val,
+                             const T *__restrict__ invd_row, int unit_diag, T *__restrict__ ovf_val) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= npad * 32) return;
+    const int64_t st = t >> 5;
+    const int lane = (int)(t & 31);
+    const int4 c = reinterpret_cast<const int4 *>(ctl + (size_t)st * kCtlBytes)[lane];
+    if (c.w < 0) return;                               // padding lane
+    const int row = c.w, ka = tri_ptr[row], nd = tri_ptr[row + 1] - ka;
+    T a[kSH] = {T(0), T(0), T(0)};
+    if (nd > kSH) {
+        const int o = c.x - kOvfBase;
+        for (int q = 0; q < nd; ++q) ovf_val[o + q] = tri_val[ka + q];
+    } else {
+        for (int q = 0; q < nd; ++q) a[q] = tri_val[ka + q];
+    }
+    unsigned char *fr = coef + (size_t)st * Coef<T>::BYTES;
+    const int4 pub = reinterpret_cast<const int4 *>(fr + Coef<T>::PUB)[lane];
+    Coef<T>::put(fr, lane, a, unit_diag ? T(1) : invd_row[row], pub);
+}
+
 template <typename T>
 __global__ void k_fill_sentinel(T *p, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1557,6 +1583,23 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     B.nent = (int64_t)npad * (kCtlBytes + CB);
     SPTRSV_CUDA(cudaStreamSynchronize(s));
     B.built = true;
+    return SPTRSV_SUCCESS;
+}
+
+sptrsv_status_t block_refresh_values(sptrsv_handle_t h, const int32_t *tri_ptr, const void *tri_val, cudaStream_t s) {
+    const BlockPlan &B = h->block;
+    const int64_t npad = B.npad;
+    if (npad == 0) return SPTRSV_SUCCESS;
+    const int g = (int)((npad * 32 + 255) / 256);
+    if (h->dtype == SPTRSV_F64)
+        k_rec_refill<double><<<g, 256, 0, s>>>(npad, (const unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, tri_ptr,
+                                               (const double *)tri_val, (const double *)h->d_invd_row,
+                                               h->diag == SPTRSV_UNIT, (double *)B.d_ovf_val);
+    else
+        k_rec_refill<float><<<g, 256, 0, s>>>(npad, (const unsigned char *)B.d_ctl, (unsigned char *)B.d_coef, tri_ptr,
+                                              (const float *)tri_val, (const float *)h->d_invd_row,
+                                              h->diag == SPTRSV_UNIT, (float *)B.d_ovf_val);
+    SPTRSV_CUDA(cudaGetLastError());
     return SPTRSV_SUCCESS;
 }
 

@@ -255,6 +255,32 @@ sptrsv_status_t launch_column(sptrsv_handle_t h, const T *b, T *x, cudaStream_t 
 
 }  // namespace
 
+// new values (the per-position CSR already refreshed): refill the CSC (the
+// order of a column's rows follows the atomic counters, rows and values are
+// written together)
+sptrsv_status_t csc_refresh_values(sptrsv_handle_t h, cudaStream_t s) {
+    const int n = h->n;
+    DevArena tmp(s);
+    struct Guard {
+        DevArena &a;
+        ~Guard() { a.release_all(); }
+    } guard{tmp};
+    sptrsv_status_t st;
+    int32_t *cur = nullptr;
+    if ((st = tmp.alloc_n(&cur, (size_t)n + 1)) != SPTRSV_SUCCESS) return st;
+    SPTRSV_CUDA(cudaMemsetAsync(cur, 0, sizeof(int32_t) * ((size_t)n + 1), s));
+    const int g = (n + 255) / 256;
+    if (h->dtype == SPTRSV_F64)
+        k_csc_fill<double><<<g, 256, 0, s>>>(n, h->d_perm, h->d_mr_ptr, h->d_mr_col, (const double *)h->d_mr_val,
+                                             h->d_c_ptr, cur, h->d_c_row, (double *)h->d_c_val);
+    else
+        k_csc_fill<float><<<g, 256, 0, s>>>(n, h->d_perm, h->d_mr_ptr, h->d_mr_col, (const float *)h->d_mr_val,
+                                            h->d_c_ptr, cur, h->d_c_row, (float *)h->d_c_val);
+    SPTRSV_CUDA(cudaGetLastError());
+    SPTRSV_CUDA(cudaStreamSynchronize(s));
+    return SPTRSV_SUCCESS;
+}
+
 sptrsv_status_t column_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s) {
     if (h->n == 0) return SPTRSV_SUCCESS;
     if (h->dtype == SPTRSV_F64)

@@ -163,6 +163,15 @@ struct sptrsv_handle_s {
 
 namespace sptrsv {
 void keep_pool_memory(int dev);
+sptrsv_status_t update_values_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
+                                   const void *vals, cudaStream_t s);                      // analyze.cu
+// new values into every derived layout the handle has built (from its level-ordered layout)
+sptrsv_status_t refresh_derived_values(sptrsv_handle_t h, cudaStream_t s);                 // solve.cu
+sptrsv_status_t block_refresh_values(sptrsv_handle_t h, const int32_t *tri_ptr, const void *tri_val,
+                                     cudaStream_t s);                                       // block.cu
+sptrsv_status_t mrt_refresh_values(sptrsv_handle_t h, const int32_t *tri_ptr, const void *tri_val,
+                                   cudaStream_t s);                                         // mrt.cu
+sptrsv_status_t csc_refresh_values(sptrsv_handle_t h, cudaStream_t s);                      // column.cu
 sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
                              const void *vals, cudaStream_t s);
 sptrsv_status_t solve_impl(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);

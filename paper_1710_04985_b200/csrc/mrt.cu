@@ -456,6 +456,19 @@ __global__ void k_mrt_wfill(int m, int K, const uint32_t *skey, const int32_t *s
     atomicMax(&waits[u].y, wneed[sperm[o]]);
 }
 
+// new values into the records (NEXT-2 value update): slots kept, a[d] and 1/d re-read
+template <typename T>
+__global__ void k_mrt_refill(int n, unsigned char *rec, const int32_t *__restrict__ tri_ptr,
+                             const T *__restrict__ tri_val, const T *__restrict__ invd_row, int unit_diag) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    unsigned char *r = rec + (size_t)p * rec_bytes<T>();
+    const int4 h0 = reinterpret_cast<const int4 *>(r)[0];
+    T *ar = reinterpret_cast<T *>(r + 32);
+    for (int d = 0; d < h0.y; ++d) ar[d] = tri_val[tri_ptr[h0.x] + d];
+    ar[kMaxDeps] = unit_diag ? T(1) : invd_row[h0.x];
+}
+
 int i32_read(const int32_t *d, int64_t i, cudaStream_t s, sptrsv_status_t &st) {
     int32_t v = 0;
     cudaError_t e = cudaMemcpyAsync(&v, d + i, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
@@ -709,6 +722,19 @@ sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrh
                                                 smem_of(h->dtype, cpl), s));
     }
     h->last_solve = 2;
+    return SPTRSV_SUCCESS;
+}
+
+sptrsv_status_t mrt_refresh_values(sptrsv_handle_t h, const int32_t *tri_ptr, const void *tri_val, cudaStream_t s) {
+    const MrtPlan &M = h->mrt;
+    const int g = (h->n + 255) / 256;
+    if (h->dtype == SPTRSV_F64)
+        k_mrt_refill<double><<<g, 256, 0, s>>>(h->n, M.d_rec, tri_ptr, (const double *)tri_val,
+                                               (const double *)h->d_invd_row, h->diag == SPTRSV_UNIT);
+    else
+        k_mrt_refill<float><<<g, 256, 0, s>>>(h->n, M.d_rec, tri_ptr, (const float *)tri_val,
+                                              (const float *)h->d_invd_row, h->diag == SPTRSV_UNIT);
+    SPTRSV_CUDA(cudaGetLastError());
     return SPTRSV_SUCCESS;
 }
 

@@ -707,6 +707,35 @@ sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream
 
 }  // namespace
 
+sptrsv_status_t refresh_derived_values(sptrsv_handle_t h, cudaStream_t s) {
+    sptrsv_status_t st;
+    if (h->mr_built) {                        // per-position CSR: same positions, new values
+        const int grid = std::max(1, std::min((h->nchunks * 32 + 255) / 256, h->num_sms * 16));
+        if (h->dtype == SPTRSV_F64)
+            k_mr_fill<double><<<grid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_ecol, (const double *)h->d_eval,
+                                                   h->d_mr_ptr, h->d_mr_col, (double *)h->d_mr_val);
+        else
+            k_mr_fill<float><<<grid, 256, 0, s>>>(h->nchunks, h->d_chunks, h->d_ecol, (const float *)h->d_eval,
+                                                  h->d_mr_ptr, h->d_mr_col, (float *)h->d_mr_val);
+        SPTRSV_CUDA(cudaGetLastError());
+        if (h->csc_built && (st = csc_refresh_values(h, s)) != SPTRSV_SUCCESS) return st;
+    }
+    if (h->block.built || h->mrt.built) {
+        DevArena tmp(s);
+        struct Guard {
+            DevArena &a;
+            ~Guard() { a.release_all(); }
+        } guard{tmp};
+        int32_t *tri_ptr = nullptr, *tri_col = nullptr;
+        void *tri_val = nullptr;
+        if ((st = build_tri_csr(h, tmp, s, &tri_ptr, &tri_col, &tri_val)) != SPTRSV_SUCCESS) return st;
+        if (h->block.built && (st = block_refresh_values(h, tri_ptr, tri_val, s)) != SPTRSV_SUCCESS) return st;
+        if (h->mrt.built && (st = mrt_refresh_values(h, tri_ptr, tri_val, s)) != SPTRSV_SUCCESS) return st;
+        SPTRSV_CUDA(cudaStreamSynchronize(s));      // before the temporaries are released
+    }
+    return SPTRSV_SUCCESS;
+}
+
 sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s) {
     return h->dtype == SPTRSV_F64 ? build_mr<double>(h, s) : build_mr<float>(h, s);
 }

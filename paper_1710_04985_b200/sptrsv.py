@@ -62,6 +62,8 @@ def _load():
     lib.sptrsv_solve_host.argtypes = [vp, vp, vp, i32, vp]
     lib.sptrsv_destroy.restype = ctypes.c_int
     lib.sptrsv_destroy.argtypes = [vp]
+    lib.sptrsv_update_values.restype = ctypes.c_int
+    lib.sptrsv_update_values.argtypes = [vp, vp, vp, vp, vp]
     lib.sptrsv_set_algo.restype = ctypes.c_int
     lib.sptrsv_set_algo.argtypes = [vp, ctypes.c_int]
     lib.sptrsv_get_info.restype = ctypes.c_int
@@ -117,6 +119,10 @@ def sptrsv_solve_host(handle, b_ptr, x_ptr, nrhs, stream_ptr) -> int:
 
 def sptrsv_destroy(handle) -> int:
     return _lib.sptrsv_destroy(handle)
+
+
+def sptrsv_update_values(handle, rowptr_ptr, colidx_ptr, vals_ptr, stream_ptr) -> int:
+    return _lib.sptrsv_update_values(handle, rowptr_ptr, colidx_ptr, vals_ptr, stream_ptr)
 
 
 def sptrsv_set_algo(handle, algo) -> int:
@@ -190,6 +196,22 @@ class TriangularSolver:
             raise SptrsvError(st, "sptrsv_analyze", info)
         if algo != "self":
             self.set_algo(algo)
+
+    def update_values(self, rowptr, colidx, vals, stream=None):
+        """New values for the analyzed pattern (same rowptr / colidx CUDA tensors'
+        contents); raises SptrsvError (INVALID_VALUE: another pattern) and keeps
+        the old values on failure."""
+        import torch
+        for t in (rowptr, colidx):
+            if t.dtype != torch.int32 or not t.is_cuda or not t.is_contiguous():
+                raise TypeError("rowptr/colidx must be contiguous int32 CUDA tensors")
+        if rowptr.numel() != self.n + 1:
+            raise ValueError(f"rowptr must have n + 1 = {self.n + 1} entries")
+        if vals is not None and (vals.dtype != self.torch_dtype or not vals.is_cuda or not vals.is_contiguous()):
+            raise TypeError("vals must be a contiguous CUDA tensor of the handle's dtype")
+        st = sptrsv_update_values(self.handle, _dptr(rowptr), _dptr(colidx), _dptr(vals), _stream_ptr(stream))
+        if st != 0:
+            raise SptrsvError(st, "sptrsv_update_values")
 
     def set_algo(self, algo: str):
         st = sptrsv_set_algo(self.handle, ALGOS[algo])

@@ -66,6 +66,7 @@ def test_host_side_argument_checks(S):
     assert S.sptrsv_get_levels(None, None, None, None) == 1
     assert S.sptrsv_get_dep_counts(None, None) == 1
     assert S.sptrsv_get_info(None)[0] == 1
+    assert S.sptrsv_update_values(None, None, None, None, None) == 1
     assert S.sptrsv_destroy(None) == 0
 
 

@@ -704,3 +704,78 @@ def test_mrhs_tile_kernel_timeout_then_clean(S):
     X2 = sv.solve(B).cpu().numpy()
     assert sv.solve_status() == "SUCCESS"
     assert np.array_equal(X, X2)
+
+
+# ------------------------------------------------------------ value update (NEXT-2)
+def _dev(m, dtype):
+    rp = torch.from_numpy(np.ascontiguousarray(m.rowptr, dtype=np.int32)).cuda()
+    ci = torch.from_numpy(np.ascontiguousarray(m.colidx, dtype=np.int32)).cuda()
+    va = torch.from_numpy(np.ascontiguousarray(m.vals, dtype=dtype)).cuda()
+    return rp, ci, va
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["7pt_lower", "27pt_ilu_upper", "random_unit_lower"])
+def test_update_values_equals_fresh_analysis(S, case, dtype):
+    """sptrsv_update_values on a handle that has built every layout (level
+    rows, BLOCK records, multi-RHS tile / value-as-flag / level, CSC): every
+    algorithm then gives bit for bit the result of a fresh analysis of the new
+    values, and matches the oracle."""
+    rng = np.random.default_rng(11)
+    if case == "7pt_lower":
+        m, uplo, diag = workloads.stencil((32, 24, 16), 7, "lower"), "lower", "non_unit"
+    elif case == "27pt_ilu_upper":
+        m, uplo, diag = workloads.ilu0(workloads.stencil((14, 12, 10), 27)), "upper", "non_unit"
+    else:
+        m, uplo, diag = random_lowdeg(20000, 5, "lower"), "lower", "unit"
+    m2 = workloads.CSR(m.n, m.rowptr, m.colidx, m.vals * rng.uniform(0.5, 1.5, size=m.vals.size))
+    b1 = workloads.rhs(m.n, 1, seed=3)[:, 0].astype(dtype)
+    B = workloads.rhs(m.n, 32, seed=4).astype(dtype)
+    rp, ci, va = _dev(m, dtype)
+    _, _, va2 = _dev(m2, dtype)
+    sv = S.TriangularSolver(m.n, rp, ci, va, uplo, diag, "auto")
+    algos = ["self", "level", "block", "slfc", "levc", "auto"]
+    if case == "27pt_ilu_upper":
+        algos.remove("block")                      # refused on natural partitions with > 3 deps per row
+    bt, Bt = torch.from_numpy(b1).cuda(), torch.from_numpy(B).cuda()
+    for algo in algos:                             # build every layout on the old values
+        sv.set_algo(algo)
+        sv.solve(bt)
+        sv.solve(Bt)
+    sv.update_values(rp, ci, va2)
+    fresh = S.TriangularSolver(m.n, rp, ci, va2, uplo, diag, "self")
+    ref = oracle.solve(m2.astype(dtype), b1, uplo, diag, dtype=dtype)
+    for algo in algos:
+        sv.set_algo(algo)
+        fresh.set_algo(algo)
+        x = sv.solve(bt).cpu().numpy()
+        assert sv.solve_status() == "SUCCESS"
+        assert relerr(x, ref) <= TOL[dtype], algo
+        if algo not in ("slfc", "levc"):          # atomics: order varies run to run
+            assert np.array_equal(x, fresh.solve(bt).cpu().numpy()), algo
+            assert np.array_equal(sv.solve(Bt).cpu().numpy(), fresh.solve(Bt).cpu().numpy()), algo
+
+
+def test_update_values_rejects_other_pattern_and_keeps_values(S):
+    m = workloads.stencil((16, 16, 8), 7, "lower")
+    rp, ci, va = _dev(m, np.float64)
+    sv = S.TriangularSolver(m.n, rp, ci, va, "lower", "non_unit", "auto")
+    b = torch.from_numpy(workloads.rhs(m.n, 1, seed=1)[:, 0]).cuda()
+    x0 = sv.solve(b).cpu().numpy()
+    # another pattern: drop the last off-diagonal entry of row 100 (moved into the upper part)
+    ci2 = ci.clone()
+    k = int(m.rowptr[101]) - 2                      # an off-diagonal of row 100 (diagonal last)
+    ci2[k] = 100 + 1
+    ci_sorted = ci2.cpu().numpy()
+    row = ci_sorted[m.rowptr[100]:m.rowptr[101]]
+    ci_sorted[m.rowptr[100]:m.rowptr[101]] = np.sort(row)
+    with pytest.raises(S.SptrsvError) as e:
+        sv.update_values(rp, torch.from_numpy(ci_sorted).cuda(), va)
+    assert e.value.name == "INVALID_VALUE"
+    # a zero pivot: ZERO_PIVOT, values kept
+    va0 = va.clone()
+    va0[int(m.rowptr[7]) + (int(m.rowptr[8]) - int(m.rowptr[7])) - 1] = 0.0   # diagonal of row 7 (last in its row)
+    with pytest.raises(S.SptrsvError) as e:
+        sv.update_values(rp, ci, va0)
+    assert e.value.name == "ZERO_PIVOT"
+    assert np.array_equal(sv.solve(b).cpu().numpy(), x0)
