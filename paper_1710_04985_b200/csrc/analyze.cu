@@ -362,6 +362,26 @@ __global__ void k_dep_fill(int n, const int32_t *__restrict__ rowptr, const int3
             if (in_tri(i, j, uplo)) crow[cptr[j] + atomicAdd(&cur[j], 1)] = i;
         }
 }
+// One round of the paper's host-driven Kahn (FIND_LEVEL): the
+// rows of frontier level l get lev = l and release their dependents into the
+// next frontier; the host launches one round per level and reads the next
+// frontier's size back (analysis-mode study, NEXT-2; the default analysis runs
+// all rounds in one cooperative launch, k_kahn below).
+__global__ void k_kahn_round(int nf, int l, const int32_t *__restrict__ cptr, const int32_t *__restrict__ crow,
+                             int32_t *indeg, const int32_t *__restrict__ Fc, int32_t *Fn, int32_t *cnt_next,
+                             int32_t *lev) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwp = (gridDim.x * blockDim.x) >> 5;
+    for (int idx = gw; idx < nf; idx += nwp) {
+        const int i = Fc[idx];
+        if (lane == 0) lev[i] = l;
+        const int k1 = cptr[i + 1];
+        for (int k = cptr[i] + lane; k < k1; k += 32) {
+            const int r = crow[k];
+            if (atomicSub(&indeg[r], 1) == 1) Fn[atomicAdd(cnt_next, 1)] = r;
+        }
+    }
+}
 __global__ void k_frontier0(int n, const int32_t *__restrict__ dp, int32_t *F, int32_t *cnt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && dp[i] == 0) F[atomicAdd(cnt, 1)] = i;
@@ -554,6 +574,11 @@ static int grid_for(int64_t items, int per_block, int cap) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
 }
 
+// Level computation of the analysis (debug / study setting, process-wide):
+// 0 Kahn by rounds in one cooperative launch (default), 1 the sync-free
+// value-as-flag kernel, 2 the paper's host loop with one launch per level.
+int g_levels_mode = 0;
+
 // ------------------------------------------------------------- driver
 sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
                              const void *vals, cudaStream_t s) {
@@ -620,8 +645,8 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
     if ((st = tmp.alloc_n(&d_ticket, 1)) != SPTRSV_SUCCESS) return st;
     SPTRSV_CUDA(cudaMemsetAsync(d_ticket, 0, sizeof(unsigned), s));
     SPTRSV_CUDA(cudaMemsetAsync(h->d_lev, 0xFF, sizeof(int32_t) * (size_t)n, s));
-    const char *esf = getenv("SPTRSV_LEVELS_SYNCFREE");     // 1: the sync-free k_levels
-    if (esf && *esf == '1') {
+    const int mode = g_levels_mode;                          // sptrsv_dbg_levels_mode (analysis study)
+    if (mode == 1) {
         k_levels<<<grid_for(((int64_t)n + 31) / 32 * 32, 256, h->num_sms * 8), 256, 0, s>>>(
             n, rowptr, colidx, h->uplo, h->d_lev, d_ticket, d_stat);
     } else {
@@ -650,12 +675,35 @@ sptrsv_status_t analyze_impl(sptrsv_handle_t h, const int32_t *rowptr, const int
         SPTRSV_CUDA(cudaMemcpyAsync(indeg, h->d_dp, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
         k_frontier0<<<(n + 255) / 256, 256, 0, s>>>(n, h->d_dp, F0, fcnt);
         SPTRSV_CUDA(cudaGetLastError());
-        int per_sm = 0;
-        SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kahn, kKahnThreads, 0));
-        const int kg = std::max(1, std::min(per_sm, 1)) * h->num_sms;
-        void *args[] = {(void *)&n, (void *)&cptr, (void *)&crow, (void *)&indeg, (void *)&F0, (void *)&F1,
-                        (void *)&fcnt, (void *)&h->d_lev, (void *)&kbar, (void *)&d_stat};
-        SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_kahn, kg, kKahnThreads, args, 0, s));
+        if (mode == 2) {
+            // the paper's host loop: one launch per level, the frontier size read back each time
+            int nf = 0, l = 0;
+            SPTRSV_CUDA(cudaMemcpyAsync(&nf, fcnt, sizeof(int), cudaMemcpyDeviceToHost, s));
+            SPTRSV_CUDA(cudaStreamSynchronize(s));
+            while (nf > 0) {
+                int32_t *Fc = (l & 1) ? F1 : F0, *Fn = (l & 1) ? F0 : F1;
+                int32_t *cn = fcnt + ((l + 1) & 1);
+                SPTRSV_CUDA(cudaMemsetAsync(cn, 0, sizeof(int32_t), s));
+                k_kahn_round<<<grid_for((int64_t)nf * 32, 256, h->num_sms * 8), 256, 0, s>>>(nf, l, cptr, crow, indeg,
+                                                                                           Fc, Fn, cn, h->d_lev);
+                SPTRSV_CUDA(cudaGetLastError());
+                SPTRSV_CUDA(cudaMemcpyAsync(&nf, cn, sizeof(int), cudaMemcpyDeviceToHost, s));
+                SPTRSV_CUDA(cudaStreamSynchronize(s));
+                ++l;
+            }
+            AnalysisStatus hl;
+            SPTRSV_CUDA(cudaMemcpyAsync(&hl, d_stat, sizeof(hl), cudaMemcpyDeviceToHost, s));
+            SPTRSV_CUDA(cudaStreamSynchronize(s));
+            hl.max_lev = l - 1;
+            SPTRSV_CUDA(cudaMemcpyAsync(d_stat, &hl, sizeof(hl), cudaMemcpyHostToDevice, s));
+        } else {
+            int per_sm = 0;
+            SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_kahn, kKahnThreads, 0));
+            const int kg = std::max(1, std::min(per_sm, 1)) * h->num_sms;
+            void *args[] = {(void *)&n, (void *)&cptr, (void *)&crow, (void *)&indeg, (void *)&F0, (void *)&F1,
+                            (void *)&fcnt, (void *)&h->d_lev, (void *)&kbar, (void *)&d_stat};
+            SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_kahn, kg, kKahnThreads, args, 0, s));
+        }
     }
     SPTRSV_CUDA(cudaGetLastError());
     SPTRSV_CUDA(cudaMemcpyAsync(&hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s));

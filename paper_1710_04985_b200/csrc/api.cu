@@ -263,6 +263,15 @@ extern "C" const char *sptrsv_last_cuda_error(void) { return sptrsv::g_last_cuda
 // ---------------------------------------------------------------- debug hooks
 // Not part of include/sptrsv.h: test and profiling instrumentation.
 
+// Level computation of later analyses (process-wide, for the analysis-cost
+// study and tests): 0 Kahn by rounds in one cooperative kernel (default),
+// 1 the sync-free kernel, 2 one launch per level from a host loop.
+extern "C" int sptrsv_dbg_levels_mode(int mode) {
+    if (mode < 0 || mode > 2) return SPTRSV_ERR_INVALID_VALUE;
+    sptrsv::g_levels_mode = mode;
+    return SPTRSV_SUCCESS;
+}
+
 // Multi-RHS kernel selection for A/B measurements: 0 automatic, 1 never the
 // tile kernel (value-as-flag / level-scheduled kernels only).
 extern "C" int sptrsv_dbg_mrhs_path(sptrsv_handle_t h, int mode) {

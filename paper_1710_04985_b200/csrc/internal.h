@@ -163,6 +163,7 @@ struct sptrsv_handle_s {
 
 namespace sptrsv {
 void keep_pool_memory(int dev);
+extern int g_levels_mode;                    // analyze.cu (sptrsv_dbg_levels_mode)
 sptrsv_status_t update_values_impl(sptrsv_handle_t h, const int32_t *rowptr, const int32_t *colidx,
                                    const void *vals, cudaStream_t s);                      // analyze.cu
 // new values into every derived layout the handle has built (from its level-ordered layout)

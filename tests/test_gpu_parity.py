@@ -597,17 +597,23 @@ def test_multi_rhs_value_as_flag(S, nrhs, uplo, diag, dtype):
 
 
 @pytest.mark.parametrize("uplo", ["lower", "upper"])
-def test_levels_kahn_and_syncfree_agree(S, uplo, monkeypatch):
-    """Both level computations (Kahn by rounds, default; sync-free k_levels,
-    SPTRSV_LEVELS_SYNCFREE=1) give the oracle's levels bit for bit."""
+def test_levels_kahn_and_syncfree_agree(S, uplo):
+    """All three level computations (Kahn by rounds in one cooperative launch,
+    default; the sync-free kernel; the paper's host loop with one launch per
+    level) give the oracle's levels bit for bit."""
+    import ctypes
+    lib = ctypes.CDLL(S.LIB_PATH)
     m = random_triangular_fast(20000, 6.0, 11, uplo)
     ref = oracle.analyze(m, uplo, "non_unit")
-    for env in ("0", "1"):
-        monkeypatch.setenv("SPTRSV_LEVELS_SYNCFREE", env)
-        lev, ilev, jlev, nlev = S.from_csr(m, uplo).levels()
-        assert nlev == ref["nlev"]
-        assert np.array_equal(lev, ref["lev"]) and np.array_equal(jlev, ref["jlev"])
-        assert np.array_equal(ilev, ref["ilev"])
+    try:
+        for mode in (0, 1, 2):
+            assert lib.sptrsv_dbg_levels_mode(mode) == 0
+            lev, ilev, jlev, nlev = S.from_csr(m, uplo).levels()
+            assert nlev == ref["nlev"]
+            assert np.array_equal(lev, ref["lev"]) and np.array_equal(jlev, ref["jlev"])
+            assert np.array_equal(ilev, ref["ilev"])
+    finally:
+        lib.sptrsv_dbg_levels_mode(0)
 
 
 # ------------------------------------------------------------ multi-RHS tile kernel (mrt.cu)
