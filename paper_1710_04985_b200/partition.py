@@ -21,6 +21,24 @@ def block_range(total: int, world_size: int, rank: int) -> tuple[int, int]:
     return start, stop
 
 
+def factor_assignment(weights, world_size: int) -> list[list[int]]:
+    """Independent factors (NEXT-4) over the ranks: longest-processing-time
+    greedy on the per-factor weights (e.g. nnz): factors in decreasing weight
+    (ties by index) go to the least-loaded rank (ties: lowest rank).
+    Deterministic; every factor is owned by exactly one rank; the maximum load
+    is at most the mean load plus the largest weight."""
+    if world_size < 1:
+        raise ValueError("bad partition arguments")
+    order = sorted(range(len(weights)), key=lambda i: (-weights[i], i))
+    load = [0.0] * world_size
+    owned: list[list[int]] = [[] for _ in range(world_size)]
+    for i in order:
+        r = min(range(world_size), key=lambda q: (load[q], q))
+        owned[r].append(i)
+        load[r] += float(weights[i])
+    return [sorted(o) for o in owned]
+
+
 def all_ranges(total: int, world_size: int) -> list[tuple[int, int]]:
     return [block_range(total, world_size, r) for r in range(world_size)]
 

@@ -86,3 +86,32 @@ def test_break_even_solves_matches_brute_force():
             assert got is None or got >= 200000, (sa, ta, sb, tb, got)
         else:
             assert got == want, (sa, ta, sb, tb, got, want)
+
+
+@pytest.mark.parametrize("ws", [1, 2, 3, 4, 8])
+def test_factor_assignment_covers_and_balances(ws):
+    import random
+    rng = random.Random(ws)
+    for _ in range(50):
+        w = [rng.randint(1, 1000) for _ in range(rng.randint(0, 40))]
+        own = partition.factor_assignment(w, ws)
+        assert len(own) == ws
+        flat = sorted(i for o in own for i in o)
+        assert flat == list(range(len(w)))                 # each factor exactly once
+        loads = [sum(w[i] for i in o) for o in own]
+        if w:
+            assert max(loads) <= sum(w) / ws + max(w)       # LPT bound
+        assert own == partition.factor_assignment(w, ws)    # deterministic
+
+
+def test_block_jacobi_workload_is_block_diagonal_ilu():
+    import numpy as np
+    import workloads
+    t = workloads.slab_thicknesses(32, 5, seed=6)
+    assert sum(t) == 32 and min(t) >= 1 and len(t) == 5
+    blocks = workloads.block_jacobi_ilu0((6, 5, 32), 27, 5, seed=6)
+    assert [b.n for b in blocks] == [6 * 5 * tz for tz in t]
+    # each block is the ILU(0) of its own slab's stencil: same pattern as the slab matrix
+    for b, tz in zip(blocks, t):
+        a = workloads.stencil((6, 5, tz), 27, "full")
+        assert np.array_equal(b.rowptr, a.rowptr) and np.array_equal(b.colidx, a.colidx)

@@ -187,6 +187,26 @@ CONFIGS = {
 SEEDS = {1: 1, 2: 2, 3: 3, 4: 4, 5: 1000}
 
 
+def slab_thicknesses(nz: int, nblocks: int, seed: int) -> list[int]:
+    """Thicknesses (>= 1) of ``nblocks`` z-slabs summing to ``nz``: a seeded
+    random composition (uneven subdomains, so the batch partition matters)."""
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(0.5, 1.5, size=nblocks)
+    t = np.maximum(1, np.floor(w / w.sum() * nz).astype(int))
+    t[int(np.argmax(t))] += nz - int(t.sum())
+    assert t.min() >= 1 and int(t.sum()) == nz
+    return [int(v) for v in t]
+
+
+def block_jacobi_ilu0(dims=(128, 128, 128), points: int = 27, nblocks: int = 16, seed: int = 6) -> list:
+    """NEXT-4 workload: a block-Jacobi preconditioner of the ``points``-point
+    Laplacian on ``dims``, split into ``nblocks`` z-slabs (couplings between
+    slabs dropped); each block's ILU(0) (IKJ, reading Q19) as one combined CSR
+    -- independent factors, each solved as the Eq. (3) pair (unit L, then U)."""
+    nx, ny, nz = dims
+    return [ilu0(stencil((nx, ny, t), points, "full")) for t in slab_thicknesses(nz, nblocks, seed)]
+
+
 def config(k: int, scale: float = 1.0):
     """Matrix for configuration ``k``.  ``scale`` < 1 shrinks the grid / n for
     fast tests (same recipe).  Returns (CSR, dict of solve parameters)."""
@@ -209,4 +229,8 @@ def config(k: int, scale: float = 1.0):
         m, lev = powerlaw(n, nlev, seed=4)
         m.meta["lev"] = lev
         return m, {"uplo": "lower", "diag": "non_unit", "nrhs": 1, "seed": 5}
+    if k == 6:
+        g = max(4, int(round(128 * scale)))
+        blocks = block_jacobi_ilu0((g, g, g), 27, 16, seed=6)
+        return blocks, {"pair": True, "seed": 7, "blocks": True}
     raise KeyError(k)
