@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kColThreads) k_slfc(int n, const int32_t *__re
                                                       const int32_t *__restrict__ cptr,
                                                       const int32_t *__restrict__ crow,
                                                       const T *__restrict__ cval, T *x, int32_t *count,
-                                                      unsigned *ctr, unsigned nwarps_total, int rel_each) {
+                                                      unsigned *ctr, unsigned nwarps_total) {
     const int lane = threadIdx.x & 31;
     const int nblk = (n + 31) / 32;
     for (;;) {
@@ -122,14 +122,11 @@ __global__ void __launch_bounds__(kColThreads) k_slfc(int n, const int32_t *__re
             const int k0 = cptr[i], k1 = cptr[i + 1];
             column_update<T, UNIT>(i, invd_row, cptr, crow, cval, x);
             if (k1 > k0) {
-                if (rel_each) {        // release on every decrement instead of one fence
-                    for (int k = k0; k < k1; ++k)
-                        asm volatile("red.release.gpu.global.add.s32 [%0], -1;" ::"l"(count + crow[k]) : "memory");
-                } else {
-                    // the x updates above happen before any counter decrement below
-                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-                    for (int k = k0; k < k1; ++k) red_dec(count + crow[k]);
-                }
+                // the x updates above happen before any counter decrement below
+                // (one fence per column; a red.release per decrement measured
+                // 2.8x slower on cfg4, round 1)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                for (int k = k0; k < k1; ++k) red_dec(count + crow[k]);
             }
         }
     }
@@ -229,15 +226,12 @@ sptrsv_status_t launch_column(sptrsv_handle_t h, const T *b, T *x, cudaStream_t 
             SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_slfc<T, UNIT>, kColThreads, 0));
             // at most 2 CTAs (16 warps) per SM: enough columns in flight, and
             // not so many spinning lanes that their polls slow the L2
-            const char *ec = getenv("SPTRSV_SLFC_CPS");
-            const int cps = (ec && atoi(ec) > 0) ? atoi(ec) : 1;   // 1/SM: 2-6% faster than 2
-            h->slfc_grid = std::max(1, std::min(per_sm, cps)) * h->num_sms;
+            h->slfc_grid = std::max(1, std::min(per_sm, 1)) * h->num_sms;   // 1/SM: 2-6% faster than 2
         }
         const int grid = h->slfc_grid;
         k_slfc<T, UNIT><<<grid, kColThreads, 0, s>>>(n, h->d_perm, (const T *)h->d_invd_row, h->d_c_ptr, h->d_c_row,
                                                     (const T *)h->d_c_val, x, h->d_count, h->d_ctr,
-                                                    (unsigned)(grid * (kColThreads / 32)),
-                                                    getenv("SPTRSV_SLFC_REL") ? atoi(getenv("SPTRSV_SLFC_REL")) : 0);
+                                                    (unsigned)(grid * (kColThreads / 32)));
         SPTRSV_CUDA(cudaGetLastError());
         return SPTRSV_SUCCESS;
     }
@@ -246,8 +240,7 @@ sptrsv_status_t launch_column(sptrsv_handle_t h, const T *b, T *x, cudaStream_t 
     void *args[] = {(void *)&nlev, (void *)&h->d_ilev, (void *)&h->d_perm, (void *)&h->d_invd_row,
                     (void *)&h->d_c_ptr, (void *)&h->d_c_row, (void *)&h->d_c_val, (void *)&x,
                     (void *)&h->d_bar, (void *)&h->bar_base};
-    const char *elt = getenv("SPTRSV_LEVC_THREADS");
-    const int lt = (elt && atoi(elt) >= 32 && atoi(elt) <= kLevcThreads) ? atoi(elt) / 32 * 32 : kLevcThreadsDefault;
+    const int lt = kLevcThreadsDefault;
     SPTRSV_CUDA(cudaLaunchCooperativeKernel((const void *)k_levc<T, UNIT>, grid, lt, args, 0, s));
     h->bar_base += (unsigned long long)(nlev > 0 ? nlev - 1 : 0) * grid;
     return SPTRSV_SUCCESS;
