@@ -81,7 +81,12 @@ struct MrtArgs {
     int trace_cap;
 };
 
-__device__ __forceinline__ void bar_all() { asm volatile("bar.sync 1, %0;" ::"n"(kThreadsMrt) : "memory"); }
+// bar.sync is .aligned: every lane of a warp must reach it converged (the
+// loader warp's lane-strided loops diverge: __syncwarp first)
+__device__ __forceinline__ void bar_all() {
+    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreadsMrt) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
