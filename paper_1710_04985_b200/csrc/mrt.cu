@@ -81,11 +81,13 @@ struct MrtArgs {
     int trace_cap;
 };
 
-// bar.sync is .aligned: every lane of a warp must reach it converged (the
-// loader warp's lane-strided loops diverge: __syncwarp first)
+// The loader warp and the compute warps reach the group barrier at different
+// instructions: the non-.aligned barrier.sync (bar.sync is .aligned, which
+// requires every thread of the CTA at the same instruction -- synccheck);
+// lanes reconverge first (the loader's lane-strided loops diverge)
 __device__ __forceinline__ void bar_all() {
     __syncwarp();
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreadsMrt) : "memory");
+    asm volatile("barrier.sync 1, %0;" ::"n"(kThreadsMrt) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
