@@ -782,6 +782,9 @@ __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const Bloc
     for (;;) {
         const bool p0 = is_sent(e.e0), p1 = is_sent(e.e1), p2 = is_sent(e.e2);
         if (!__any_sync(0xffffffffu, p0 || p1 || p2) || wd.expired(pa->status, pa->timeout_ns, tag)) break;
+#if SPTRSV_BLOCK_RSLEEP
+        __nanosleep(SPTRSV_BLOCK_RSLEEP);    // dev: spinning warps off the shared-memory pipe
+#endif
         if (p0) e.e0 = ext_load<T, GL>(c0, slots, gm);
         if (p1) e.e1 = ext_load<T, GL>(c1, slots, gm);
         if (p2) e.e2 = ext_load<T, GL>(c2, slots, gm);
@@ -826,6 +829,9 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
 // the CTA's steps need them.  Lane l owns items l, l+32, ...; it keeps kFw of
 // them polled at once (relaxed loads) and refills each window entry as soon
 // as its value arrived (no head-of-line blocking).
+#ifndef SPTRSV_BLOCK_RSLEEP
+#define SPTRSV_BLOCK_RSLEEP 0
+#endif
 #ifndef SPTRSV_BLOCK_FW
 #define SPTRSV_BLOCK_FW 4
 #endif
