@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6],
                     help="1-5: BASELINE.json configs; 6: NEXT-4 independent block-Jacobi ILU(0) factors over the ranks")
-    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "slfc", "levc", "auto"],
-                    help="auto: BLOCK when the analysis detects a structured grid, else SELF")
+    ap.add_argument("--algo", default="auto", choices=["self", "level", "block", "slfc", "levc", "small", "auto"],
+                    help="auto: SMALL if the triangle fits one CTA's shared memory, else BLOCK on detected "
+                         "5-/7-point grids, else SELF")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-flush", action="store_true")
@@ -101,7 +102,7 @@ def oracle_counts(m, solves, nrhs, esize):
     return sum(p[0] for p in per), sum(p[1] for p in per)
 
 
-ALGO_NAMES = {0: "self", 1: "level", 2: "block", 5: "slfc", 6: "levc"}
+ALGO_NAMES = {0: "self", 1: "level", 2: "block", 5: "slfc", 6: "levc", 7: "small"}
 
 
 def kernel_of(info, nrhs):
@@ -112,7 +113,7 @@ def kernel_of(info, nrhs):
     algo = ALGO_NAMES.get(info["algo"], "self")
     if nrhs == 1:
         return {"self": ("k_self", 2), "level": ("k_level", 1), "block": ("k_block", 1),
-                "slfc": ("k_slfc", 1), "levc": ("k_levc", 1)}[algo]
+                "slfc": ("k_slfc", 1), "levc": ("k_levc", 1), "small": ("k_small", 1)}[algo]
     if nrhs <= 16 and algo not in ("level", "levc"):
         return ("k_mrhs_vf", 2)
     es = 8 if info["dtype"] == 0 else 4
@@ -613,7 +614,7 @@ def run_ours(args):
     # extra: the other algorithms on the same problem (context, rank 0 prints)
     extra = {}
     if args.extra and world == 1:
-        for algo in ("self", "level", "block", "slfc", "levc"):
+        for algo in ("self", "level", "block", "slfc", "levc", "small"):
             if algo == args.algo:
                 continue
             try:

@@ -60,16 +60,21 @@ typedef enum {
                                hand-offs.  Any matrix on a detected structured
                                grid; otherwise only if nnz_used <= 3 n (NOT_SUPPORTED above) */
     SPTRSV_ALGO_AUTO = 3,   /* BLOCK when the analysis detects a structured grid AND every row
-                               has <= 3 dependencies (5-/7-point factors), else SELF;
-                               info.algo then reports the algorithm chosen */
+                               has <= 3 dependencies (5-/7-point factors); else SMALL when the
+                               triangle fits one CTA's shared memory (every level in one pass
+                               of 32 warps); else SELF.  info.algo reports the choice */
     /* 4: retired (round-1 CTA-tile variant); sptrsv_set_algo(4) returns INVALID_VALUE */
     SPTRSV_ALGO_SLFC = 5,   /* column-wise self-scheduled (Alg. SLFC, kernel P:631-653):
                                per-column dependency counters, x updates pushed by L2
                                atomics; last-bit results vary run to run (atomic order).
                                nrhs > 1 solves use the self-scheduled row kernels */
-    SPTRSV_ALGO_LEVC = 6    /* column-wise level-scheduled (Alg. LEVC, kernel
+    SPTRSV_ALGO_LEVC = 6,   /* column-wise level-scheduled (Alg. LEVC, kernel
                                P:536-552): atomics, grid-wide barrier per level.  nrhs > 1
                                solves use the level-scheduled row kernel */
+    SPTRSV_ALGO_SMALL = 7   /* small systems: one CTA solves level by level (LEVR)
+                               with the level-ordered triangle and x staged in shared memory.
+                               NOT_SUPPORTED if the layout does not fit one CTA's shared
+                               memory */
 } sptrsv_algo_t;
 
 typedef enum {

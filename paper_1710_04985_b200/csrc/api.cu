@@ -176,9 +176,17 @@ extern "C" sptrsv_status_t sptrsv_destroy(sptrsv_handle_t h) {
 extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo) {
     if (!h) return SPTRSV_ERR_INVALID_VALUE;
     if (algo != SPTRSV_ALGO_SELF && algo != SPTRSV_ALGO_LEVEL && algo != SPTRSV_ALGO_BLOCK &&
-        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_SLFC && algo != SPTRSV_ALGO_LEVC)
+        algo != SPTRSV_ALGO_AUTO && algo != SPTRSV_ALGO_SLFC && algo != SPTRSV_ALGO_LEVC && algo != SPTRSV_ALGO_SMALL)
         return SPTRSV_ERR_INVALID_VALUE;
     if (h->status != SPTRSV_SUCCESS) return h->status;
+    if (h->n > 0) SPTRSV_CUDA(cudaSetDevice(h->device));
+    if (algo == SPTRSV_ALGO_SMALL) {         // the whole level-ordered layout in one CTA's shared memory
+        const sptrsv_status_t st = h->n > 0 ? small_plan(h, true) : SPTRSV_ERR_NOT_SUPPORTED;
+        if (st != SPTRSV_SUCCESS) return st;
+        h->algo = SPTRSV_ALGO_SMALL;
+        h->info.algo = SPTRSV_ALGO_SMALL;
+        return SPTRSV_SUCCESS;
+    }
     // AUTO only uses BLOCK for rows with <= 3 dependencies: skip its build otherwise
     const bool want_block = algo == SPTRSV_ALGO_BLOCK || (algo == SPTRSV_ALGO_AUTO && h->info.max_row_deps <= 3);
     if (want_block && !h->block.built && h->n > 0) {
@@ -194,10 +202,15 @@ extern "C" sptrsv_status_t sptrsv_set_algo(sptrsv_handle_t h, sptrsv_algo_t algo
     if (algo == SPTRSV_ALGO_BLOCK && h->n > 0 && h->block.grid_nx == 0 && h->info.nnz_used > 3 * (int64_t)h->n)
         return SPTRSV_ERR_NOT_SUPPORTED;
     // AUTO: BLOCK on detected grids with <= 3 dependencies per row (5- / 7-point
-    // factors), SELF otherwise (27-point ILU cfg3, general matrices)
-    if (algo == SPTRSV_ALGO_AUTO)
-        algo = (h->block.built && h->block.grid_nx > 0 && h->info.max_row_deps <= 3) ? SPTRSV_ALGO_BLOCK
-                                                                                      : SPTRSV_ALGO_SELF;
+    // factors); otherwise SMALL when the triangle fits one CTA's shared memory
+    // (every level in one pass of <= 32 warps); otherwise SELF (27-point ILU
+    // cfg3, general matrices)
+    if (algo == SPTRSV_ALGO_AUTO) {
+        if (h->block.built && h->block.grid_nx > 0 && h->info.max_row_deps <= 3) algo = SPTRSV_ALGO_BLOCK;
+        else if (h->n > 0 && small_plan(h, false) == SPTRSV_SUCCESS) algo = SPTRSV_ALGO_SMALL;
+        else algo = SPTRSV_ALGO_SELF;
+        cudaGetLastError();
+    }
     h->algo = algo;
     h->info.algo = algo;
     return SPTRSV_SUCCESS;

@@ -148,6 +148,7 @@ struct sptrsv_handle_s {
     unsigned long long *d_bar = nullptr;     // level barrier counter (monotone)
     unsigned long long bar_base = 0;
     int32_t self_grid = 0, vf_grid = 0;       // resident grids (computed on first use)
+    int32_t small_threads = 0;               // SMALL: CTA size (0: no plan yet)
     // in-place / host staging
     void *d_stage = nullptr;
     size_t stage_bytes = 0;
@@ -186,7 +187,8 @@ bool mrt_eligible(sptrsv_handle_t h, const void *b, const void *x, int32_t nrhs)
 sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s);
 sptrsv_status_t mrt_solve_status(sptrsv_handle_t h);
 sptrsv_status_t column_solve(sptrsv_handle_t h, const void *b, void *x, cudaStream_t s);   // column.cu
-sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s);                            // solve.cu
+sptrsv_status_t build_mr_any(sptrsv_handle_t h, cudaStream_t s);
+sptrsv_status_t small_plan(sptrsv_handle_t h, bool explicit_request);                                              // solve.cu                            // solve.cu
 // device scans (analyze.cu)
 sptrsv_status_t exclusive_scan_i32(const int32_t *in, int32_t *out, int64_t n, DevArena &tmp, cudaStream_t s);
 sptrsv_status_t exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, DevArena &tmp, cudaStream_t s);

@@ -21,6 +21,7 @@
 // in storage order; x(i) = s * inv_d(i) (UNIT: s).  WPR rows in k_self /
 // k_level reduce lane partial sums with a fixed shuffle tree.
 #include <algorithm>
+#include <vector>
 
 #include <cstdlib>
 
@@ -525,6 +526,106 @@ __global__ void __launch_bounds__(kLevelThreads, 1) k_level_mrhs(const int32_t *
     }
 }
 
+// ---------------------------------------------------------------- SMALL
+// Small systems (SPTRSV_ALGO_SMALL; AUTO when the level-ordered layout fits in
+// shared memory): ONE CTA of 32 x (widest level's chunks) threads solves the
+// whole triangle level by level (LEVR) with the layout -- chunk
+// descriptors, level ranges, permutation, 1/d, entries -- and x staged in
+// shared memory: a level costs a CTA barrier and shared-memory latencies, not a
+// grid barrier or an L2 round trip.  The per-row arithmetic is the TPR / WPR
+// sequence of the other row kernels (bitwise equal to SELF and LEVEL).
+struct SmallLayout {
+    uint32_t off_chunks, off_levc, off_perm, off_invd, off_ecol, off_eval, off_x, bytes;
+};
+__host__ __device__ inline uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
+__host__ __device__ inline SmallLayout small_layout(int n, int nlev, int nchunks, int64_t nent, int es) {
+    SmallLayout L;
+    uint32_t o = 0;
+    L.off_chunks = o; o = align16(o + (uint32_t)nchunks * 16u);
+    L.off_levc = o;   o = align16(o + (uint32_t)(nlev + 1) * 4u);
+    L.off_perm = o;   o = align16(o + (uint32_t)n * 4u);
+    L.off_invd = o;   o = align16(o + (uint32_t)n * (uint32_t)es);
+    L.off_ecol = o;   o = align16(o + (uint32_t)nent * 4u);
+    L.off_eval = o;   o = align16(o + (uint32_t)nent * (uint32_t)es);
+    L.off_x = o;      o = align16(o + (uint32_t)n * (uint32_t)es);
+    L.bytes = o + 16u;                         // + the mbarrier
+    return L;
+}
+
+__device__ __forceinline__ void cp_async_val_s(double *dst, const double *src) { cp_async_8(dst, src); }
+__device__ __forceinline__ void cp_async_val_s(float *dst, const float *src) { cp_async_4(dst, src); }
+
+template <typename T, bool UNIT>
+__global__ void k_small(int n, int nlev, int nchunks, int64_t nent, const ChunkDesc *__restrict__ chunks,
+                        const int32_t *__restrict__ lev_chunk, const int32_t *__restrict__ perm,
+                        const T *__restrict__ invd, const int32_t *__restrict__ ecol, const T *__restrict__ eval,
+                        const T *b, T *x) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const SmallLayout L = small_layout(n, nlev, nchunks, nent, (int)sizeof(T));
+    const ChunkDesc *sc = reinterpret_cast<const ChunkDesc *>(sm + L.off_chunks);
+    const int32_t *slc = reinterpret_cast<const int32_t *>(sm + L.off_levc);
+    const int32_t *sp = reinterpret_cast<const int32_t *>(sm + L.off_perm);
+    const T *sd = reinterpret_cast<const T *>(sm + L.off_invd);
+    const int32_t *se = reinterpret_cast<const int32_t *>(sm + L.off_ecol);
+    const T *sv = reinterpret_cast<const T *>(sm + L.off_eval);
+    T *xs = reinterpret_cast<T *>(sm + L.off_x);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + L.bytes - 16u);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // the layout by TMA bulk copies (16-byte rounded: the handle's arrays are
+    // 256-byte aligned allocations), b by coalesced loads into x's slots
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t sz[6] = {align16((uint32_t)nchunks * 16u), align16((uint32_t)(nlev + 1) * 4u),
+                                align16((uint32_t)n * 4u), align16((uint32_t)n * (uint32_t)sizeof(T)),
+                                align16((uint32_t)nent * 4u), align16((uint32_t)nent * (uint32_t)sizeof(T))};
+        const void *src[6] = {chunks, lev_chunk, perm, invd, ecol, eval};
+        const uint32_t dst[6] = {L.off_chunks, L.off_levc, L.off_perm, L.off_invd, L.off_ecol, L.off_eval};
+        uint32_t tot = 0;
+        for (int i = 0; i < 6; ++i) tot += sz[i];
+        mbar_arrive_expect_tx(bar, tot);
+        for (int i = 0; i < 6; ++i)
+            if (sz[i]) bulk_g2s(sm + dst[i], src[i], sz[i], bar);
+    }
+    // b: one cp.async per element, all in flight at once (a load/store loop of
+    // a 32-thread CTA serialised ~n/32 DRAM round trips)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async_val_s(xs + i, b + i);
+    cp_async_commit();
+    cp_async_wait<0>();
+    mbar_wait(bar, 0);
+    __syncthreads();
+    for (int l = 0; l < nlev; ++l) {
+        for (int c = slc[l] + w; c < slc[l + 1]; c += nw) {
+            const ChunkDesc cd = sc[c];
+            const int width = chunk_width(cd.meta);
+            if (!chunk_wpr(cd.meta)) {
+                if (lane < chunk_nrows(cd.meta)) {
+                    const int row = sp[cd.pos + lane];
+                    T s = xs[row];
+                    for (int k = 0; k < width; ++k) {
+                        const int j = se[cd.eptr + (int64_t)k * 32 + lane];
+                        if (j < 0) break;
+                        s = fnma(sv[cd.eptr + (int64_t)k * 32 + lane], xs[j], s);
+                    }
+                    xs[row] = finish<T, UNIT>(s, sd[cd.pos + lane]);
+                }
+            } else {
+                const int row = sp[cd.pos];
+                T acc = T(0);
+                for (int k = lane; k < width; k += 32) acc = __fma_rn(sv[cd.eptr + k], xs[se[cd.eptr + k]], acc);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0) xs[row] = finish<T, UNIT>(xs[row] - acc, sd[cd.pos]);
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xs[i];
+}
+
 // per-position CSR of the referenced strict triangle (multi-RHS layout)
 __global__ void k_mr_deg(int n, const int32_t *perm, const int32_t *dp, int32_t *deg) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -628,6 +729,14 @@ constexpr int kLevelMax = 128;   // widest column block of the level-scheduled m
 template <typename T, bool UNIT>
 sptrsv_status_t launch(sptrsv_handle_t h, const T *b, T *x, int nrhs, cudaStream_t s) {
     if (h->nchunks == 0) return SPTRSV_SUCCESS;
+    if (nrhs == 1 && h->algo == SPTRSV_ALGO_SMALL) {
+        const SmallLayout L = small_layout(h->n, h->info.nlev, h->nchunks, h->nent, (int)sizeof(T));
+        k_small<T, UNIT><<<1, h->small_threads, L.bytes, s>>>(h->n, h->info.nlev, h->nchunks, h->nent, h->d_chunks,
+                                                              h->d_lev_chunk, h->d_perm, (const T *)h->d_invd,
+                                                              h->d_ecol, (const T *)h->d_eval, b, x);
+        SPTRSV_CUDA(cudaGetLastError());
+        return SPTRSV_SUCCESS;
+    }
     if (nrhs == 1 && h->algo == SPTRSV_ALGO_LEVEL) {
         const int grid = h->num_sms;
         const int nlev = h->info.nlev;
@@ -733,6 +842,29 @@ sptrsv_status_t refresh_derived_values(sptrsv_handle_t h, cudaStream_t s) {
         if (h->mrt.built && (st = mrt_refresh_values(h, tri_ptr, tri_val, s)) != SPTRSV_SUCCESS) return st;
         SPTRSV_CUDA(cudaStreamSynchronize(s));      // before the temporaries are released
     }
+    return SPTRSV_SUCCESS;
+}
+
+// SMALL plan: the layout fits in one CTA's shared memory; threads = 32 x the
+// most chunks of one level (<= 32 warps).  NOT_SUPPORTED if it does not fit,
+// or (AUTO) if some level needs more than one pass of 32 warps.
+sptrsv_status_t small_plan(sptrsv_handle_t h, bool explicit_request) {
+    if (h->small_threads > 0) return SPTRSV_SUCCESS;
+    if (h->n == 0 || h->nchunks == 0) return SPTRSV_ERR_NOT_SUPPORTED;
+    int max_smem = 0;
+    SPTRSV_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    const SmallLayout L = small_layout(h->n, h->info.nlev, h->nchunks, h->nent, (int)h->esize);
+    if ((int64_t)L.bytes > max_smem - 1024 || h->nent > (1 << 26)) return SPTRSV_ERR_NOT_SUPPORTED;
+    std::vector<int32_t> lc((size_t)h->info.nlev + 1);
+    SPTRSV_CUDA(cudaMemcpy(lc.data(), h->d_lev_chunk, sizeof(int32_t) * lc.size(), cudaMemcpyDeviceToHost));
+    int mc = 1;
+    for (int l = 0; l < h->info.nlev; ++l) mc = std::max(mc, lc[l + 1] - lc[l]);
+    if (!explicit_request && mc > 32) return SPTRSV_ERR_NOT_SUPPORTED;   // AUTO: every level in one pass of <= 32 warps
+    const int threads = 32 * std::min(mc, 32);
+    void *k = h->dtype == SPTRSV_F64 ? (h->diag == SPTRSV_UNIT ? (void *)k_small<double, true> : (void *)k_small<double, false>)
+                                     : (h->diag == SPTRSV_UNIT ? (void *)k_small<float, true> : (void *)k_small<float, false>);
+    SPTRSV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes));
+    h->small_threads = threads;
     return SPTRSV_SUCCESS;
 }
 

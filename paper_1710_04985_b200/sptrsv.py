@@ -22,9 +22,9 @@ LIB_PATH = os.environ.get("SPTRSV_DEV_LIB") or _build.LIB
 LOWER, UPPER = 0, 1
 NON_UNIT, UNIT = 0, 1
 F64, F32 = 0, 1
-ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_SLFC, ALGO_LEVC = 0, 1, 2, 3, 5, 6
+ALGO_SELF, ALGO_LEVEL, ALGO_BLOCK, ALGO_AUTO, ALGO_SLFC, ALGO_LEVC, ALGO_SMALL = 0, 1, 2, 3, 5, 6, 7
 ALGOS = {"self": ALGO_SELF, "level": ALGO_LEVEL, "block": ALGO_BLOCK, "auto": ALGO_AUTO,
-         "slfc": ALGO_SLFC, "levc": ALGO_LEVC}
+         "slfc": ALGO_SLFC, "levc": ALGO_LEVC, "small": ALGO_SMALL}
 UPLO = {"lower": LOWER, "upper": UPPER}
 DIAG = {"non_unit": NON_UNIT, "unit": UNIT}
 

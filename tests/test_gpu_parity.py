@@ -559,18 +559,54 @@ def test_column_multi_rhs_and_degenerate(S, algo):
 
 def test_auto_selection_rule(S):
     """AUTO: BLOCK on detected grids with <= 3 dependencies per row (5-/7-point
-    factors), SELF otherwise (27-point ILU, general matrices)."""
+    factors); else SMALL when the level-ordered triangle fits one CTA's shared
+    memory; else SELF (27-point ILU, general matrices)."""
     m7 = workloads.stencil((24, 20, 16), 7, "lower")
     assert S.from_csr(m7, algo="auto").info()["algo"] == 2
     m5 = workloads.stencil((40, 30), 5, "upper")
     assert S.from_csr(m5, "upper", algo="auto").info()["algo"] == 2
-    m27 = workloads.ilu0(workloads.stencil((12, 10, 8), 27, "full"))
-    for uplo, diag in (("lower", "unit"), ("upper", "non_unit")):
-        sv = S.from_csr(m27, uplo, diag, algo="auto")
-        assert sv.info()["algo"] == 0
-        b = workloads.rhs(m27.n, 1, seed=9)[:, 0]
-        x, _ = gpu_solve(S, m27, b, uplo, diag, solver=sv)
-        assert relerr(x, oracle.solve(m27, b, uplo, diag)) <= 1e-10
+    for dims, want in (((8, 6, 5), 7), ((24, 20, 16), 0)):
+        m27 = workloads.ilu0(workloads.stencil(dims, 27, "full"))
+        for uplo, diag in (("lower", "unit"), ("upper", "non_unit")):
+            sv = S.from_csr(m27, uplo, diag, algo="auto")
+            assert sv.info()["algo"] == want
+            b = workloads.rhs(m27.n, 1, seed=9)[:, 0]
+            x, _ = gpu_solve(S, m27, b, uplo, diag, solver=sv)
+            assert relerr(x, oracle.solve(m27, b, uplo, diag)) <= 1e-10
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("case", ["cfg1", "5pt_upper_unit", "random_wpr", "chain", "27pt_ilu"])
+def test_small_single_cta(S, case, dtype):
+    """SMALL (one CTA, triangle in shared memory): oracle tolerance, bitwise
+    equal to SELF and LEVEL (same per-row sequences), integer-exact cfg1."""
+    uplo, diag = "lower", "non_unit"
+    if case == "cfg1":
+        m, _ = workloads.config(1)
+    elif case == "5pt_upper_unit":
+        m, uplo, diag = workloads.stencil((40, 30), 5, "upper"), "upper", "unit"
+    elif case == "random_wpr":
+        m = random_triangular_fast(800, 2.0, 21, "lower", long_frac=0.02)       # some rows > 16 deps (WPR)
+    elif case == "chain":
+        m = chain(300)
+    else:
+        m, uplo, diag = workloads.ilu0(workloads.stencil((8, 6, 5), 27, "full")), "upper", "non_unit"
+    b = workloads.rhs(m.n, 1, seed=4)[:, 0]
+    sv = S.from_csr(m, uplo, diag, dtype, "small")
+    assert sv.info()["algo"] == 7
+    x, _ = gpu_solve(S, m, b, uplo, diag, dtype, solver=sv)
+    ref = oracle.solve(m.astype(dtype), b.astype(dtype), uplo, diag, dtype=dtype)
+    assert relerr(x, ref) <= TOL[dtype]
+    for other in ("self", "level"):
+        xo, _ = gpu_solve(S, m, b, uplo, diag, dtype, algo=other)
+        assert np.array_equal(x, xo), other
+    if case == "cfg1":
+        xt = workloads.integer_xtrue(m.n, 1, 5)[:, 0]
+        rows = np.repeat(np.arange(m.n), np.diff(m.rowptr))
+        bi = np.zeros(m.n)
+        np.add.at(bi, rows, m.vals * xt[m.colidx])
+        xi, _ = gpu_solve(S, m, bi, dtype=dtype, solver=sv)
+        assert np.array_equal(xi, xt.astype(dtype))
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
