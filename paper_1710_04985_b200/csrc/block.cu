@@ -123,11 +123,22 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 // CTA's fetcher warp, so a step only reads shared memory, every load one step
 // before its use (stage registers).  SHFL and NONE codes (< 32, 32) address
 // the zero slots, so the EXT read of every term is one unconditional LDS.
-constexpr int UB = 4;                  // steps per TMA block
+// Per-step / publication timestamps (tools/block_trace2.py, crit_path.py) are
+// compiled only into development builds: python tools/build_variant.py trace
+// -DSPTRSV_BLOCK_TRACE=1 (they cost ~10% of a step in the release loop).
+#ifndef SPTRSV_BLOCK_TRACE
+#define SPTRSV_BLOCK_TRACE 0
+#endif
+#ifndef SPTRSV_BLOCK_UB
+#define SPTRSV_BLOCK_UB 4
+#define SPTRSV_BLOCK_DG 16
+#define SPTRSV_BLOCK_DP 12
+#endif
+constexpr int UB = SPTRSV_BLOCK_UB;    // steps per TMA block
 constexpr int NCB = 8, DC = 7;         // control ring (blocks) / TMA lookahead (blocks)
 constexpr int NFB = 4, DF = 3;         // coefficient ring (blocks) / TMA lookahead (blocks)
-constexpr int DP = 12;                 // L2 prefetch lookahead (blocks), both streams
-constexpr int DG = 16;                 // b(row) loads in flight (steps): cp.async landing ring
+constexpr int DP = SPTRSV_BLOCK_DP;    // L2 prefetch lookahead (blocks), both streams
+constexpr int DG = SPTRSV_BLOCK_DG;    // b(row) loads in flight (steps): cp.async landing ring
 constexpr int UNR = 8;                 // main-loop unroll = per-warp step padding
 constexpr int XB = (DG + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
 constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
@@ -1076,7 +1087,9 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                         acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
                     }
                 }
+#if SPTRSV_BLOCK_TRACE
                 if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();   // step t's inputs present
+#endif
                 if (OVF) {
                     const bool ovf = S0.c.x >= kOvfBase && code_kind(S0.c.x) == kKNone;
                     if (__any_sync(0xffffffffu, ovf))
@@ -1085,7 +1098,9 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                 const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S0.f.invd;   // a product is never the sentinel
                 st_slot(slots_u32, S0.pub.x, xi);
                 st_mb(gm, S0.pub.y, xi);
+#if SPTRSV_BLOCK_TRACE
                 if (trc != nullptr && a.ptrace != nullptr && S0.pub.y >= 0) a.ptrace[S0.pub.y] = gtimer();
+#endif
                 if (CL) {
                     st_remote(slots_u32, S0.pub.z, xi);
                     st_remote(slots_u32, S0.pub.w, xi);
