@@ -36,7 +36,7 @@
 // One warp per tile does everything; nothing on its per-step critical chain
 // (shuffle -> select -> 3 FMA -> multiply) waits on memory:
 //   records   (codes, coefficients, publish slots) of step t+DR*UB: TMA bulk
-//             copies into a per-warp ring, L2-prefetched DP blocks ahead
+//             copies into a per-warp ring (no L2 prefetch: see SPTRSV_BLOCK_L2PF)
 //   row ids   TMA into a per-warp ring DW blocks ahead
 //   b(row)    cp.async gathers into a per-warp ring DBS steps ahead
 //   GLOB EXT  relaxed loads DG steps ahead into a register ring
@@ -128,6 +128,14 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 // -DSPTRSV_BLOCK_TRACE=1 (they cost ~10% of a step in the release loop).
 #ifndef SPTRSV_BLOCK_TRACE
 #define SPTRSV_BLOCK_TRACE 0
+#endif
+// L2 prefetch of the record streams DP blocks ahead (cp.async.bulk.prefetch):
+// off -- the TMA ring lookahead (DC = 7 blocks, ~28 steps) already covers the
+// DRAM latency, and every bulk operation costs the SM's TMA issue path: without
+// the prefetches one tile steps at 129 instead of 144 ns per level, cfg2 148.6
+// instead of 157.7 us (profiles/bench_r2d.json).
+#ifndef SPTRSV_BLOCK_L2PF
+#define SPTRSV_BLOCK_L2PF 0
 #endif
 #ifndef SPTRSV_BLOCK_UB
 #define SPTRSV_BLOCK_UB 4
@@ -980,8 +988,10 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                    UB * kCtlBytes, &cbar[kc % NCB], l0 && kc >= 0 && kc < nbx);
             tma_if(coefring + (size_t)((kf + NFB) % NFB) * UB * CB, gcoef + (size_t)kf * UB * CB, UB * CB,
                    &fbar[(kf + NFB) % NFB], l0 && kf >= 0 && kf < nbx);
-            l2pf_if(gctl + (size_t)kp * UB * kCtlBytes, UB * kCtlBytes, l0 && kp >= DP && kp < nbx);
-            l2pf_if(gcoef + (size_t)kp * UB * CB, UB * CB, l0 && kp >= DP && kp < nbx);
+            if (SPTRSV_BLOCK_L2PF) {
+                l2pf_if(gctl + (size_t)kp * UB * kCtlBytes, UB * kCtlBytes, l0 && kp >= DP && kp < nbx);
+                l2pf_if(gcoef + (size_t)kp * UB * CB, UB * CB, l0 && kp >= DP && kp < nbx);
+            }
         };
         auto wait_bar = [&](uint64_t *bar, uint32_t ph) {
             Watch wd{0, 0};
