@@ -31,6 +31,11 @@ namespace sptrsv {
 namespace {
 
 constexpr int kThreads = 256;
+// back-off between SELF poll rounds (ns)
+#ifndef SPTRSV_SELF_POLL_NS
+#define SPTRSV_SELF_POLL_NS 20
+#endif
+constexpr unsigned kSelfPollNs = SPTRSV_SELF_POLL_NS;
 
 // Debug hook (sptrsv_dbg_self_trace, not part of include/sptrsv.h): when set,
 // k_self writes %globaltimer at the publication of every row.
@@ -138,7 +143,7 @@ __device__ __forceinline__ void tpr_chunk(const ChunkDesc &cd, int lane, const i
                 done = true;
             }
             if (__all_sync(0xffffffffu, done)) return;
-            __nanosleep(20);
+            __nanosleep(kSelfPollNs);
             reload_pending<T, kTprMax>(cols, xv, x);
         }
     } else {
@@ -204,7 +209,7 @@ __device__ __forceinline__ void wpr_row(const ChunkDesc &cd, int lane, const int
         }
         if (WAIT) {
             while (pending_any<T, U>(c, v)) {       // (lazy polling measured slower here)
-                __nanosleep(20);
+                __nanosleep(kSelfPollNs);
                 reload_pending<T, U>(c, v, x);
             }
         }
