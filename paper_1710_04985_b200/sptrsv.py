@@ -298,6 +298,35 @@ class TriangularSolver:
             pass
 
 
+class StreamBatch:
+    """Independent solves (NEXT-4: independent factors, or several RHS sets)
+    issued concurrently: chain i (a list of (solver, b, x) solves run in
+    order, e.g. an Eq. (3) pair) goes to stream i % nstreams of a small pool
+    forked from and joined back into the caller's stream.  Latency-bound
+    persistent solve kernels of independent handles then share the SMs.
+    Marshalling only: each solve is an ordinary sptrsv_solve."""
+
+    def __init__(self, nstreams: int = 4):
+        import torch
+        self.streams = [torch.cuda.Stream() for _ in range(max(1, int(nstreams)))]
+
+    def run(self, chains, stream=None):
+        import torch
+        caller = stream or torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(caller)
+        for s in self.streams:
+            s.wait_event(start)
+        for i, chain in enumerate(chains):
+            s = self.streams[i % len(self.streams)]
+            for solver, b, x in chain:
+                solver.solve(b, x, stream=s)
+        for s in self.streams:
+            done = torch.cuda.Event()
+            done.record(s)
+            caller.wait_event(done)
+
+
 def from_csr(m, uplo="lower", diag="non_unit", dtype=None, algo="self", device="cuda"):
     """Upload a host CSR (workloads.CSR-like: n, rowptr, colidx, vals) and analyze it."""
     import torch

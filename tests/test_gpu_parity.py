@@ -821,3 +821,22 @@ def test_update_values_rejects_other_pattern_and_keeps_values(S):
         sv.update_values(rp, ci, va0)
     assert e.value.name == "ZERO_PIVOT"
     assert np.array_equal(sv.solve(b).cpu().numpy(), x0)
+
+
+def test_stream_batch_equals_sequential(S):
+    """NEXT-4 on one GPU: independent factor pairs issued concurrently on a
+    stream pool (StreamBatch) give the sequential results bit for bit."""
+    blocks, p = workloads.config(6, scale=0.25)
+    chains, xs, ref = [], [], []
+    for i, b in enumerate(blocks[:6]):
+        hl = S.from_csr(b, "lower", "unit", algo="auto")
+        hu = S.from_csr(b, "upper", "non_unit", algo="auto")
+        r = torch.from_numpy(workloads.rhs(b.n, 1, seed=p["seed"] + i)[:, 0]).cuda()
+        y, x = torch.empty_like(r), torch.empty_like(r)
+        chains.append([(hl, r, y), (hu, y, x)])
+        xs.append(x)
+        ref.append(hu.solve(hl.solve(r)).cpu().numpy())
+    S.StreamBatch(3).run(chains)
+    torch.cuda.synchronize()
+    for x, r in zip(xs, ref):
+        assert np.array_equal(x.cpu().numpy(), r)
