@@ -60,6 +60,43 @@ def parse():
     return ap.parse_args()
 
 
+# ------------------------------------------------------------------ process group
+def init_ranks():
+    """One process per GPU (torchrun): RANK / LOCAL_RANK / WORLD_SIZE from the
+    environment.  NCCL when every rank has its own GPU (the driver's
+    8-GPU runs); when ranks share a GPU (a test run of the multi-rank path on
+    one device) the control-plane collectives -- a barrier before and scalar
+    MAX / SUM reductions after the timed region, never on the solve path --
+    use gloo on CPU tensors."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(1, torch.cuda.device_count())
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    backend = None
+    if world > 1:
+        backend = "nccl" if world <= ndev else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local, dev, backend
+
+
+def reduce_values(vals, op, backend, dev):
+    """MAX or SUM over ranks of a few float64 scalars (outside the timed region)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+    if backend is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
 # ------------------------------------------------------------------ workload
 def build_problem(cfg: int, rank: int, world: int):
     """Matrix + RHS of a configuration (identical on every rank: seeded).
@@ -438,13 +475,7 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_1710_04985_b200 import sptrsv as S
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, local, dev, backend = init_ranks()
 
     prob = build_problem(args.config, rank, world)
     m, solves, rhs_np = prob["m"], prob["solves"], prob["rhs"]
@@ -522,20 +553,12 @@ def run_ours(args):
     solve_times = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(nh)] for e in ev]) / 1e3
     t_mean = float(times.mean())
     t_med = float(np.median(times))
-    if world > 1:
-        tt = torch.tensor([t_mean], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    else:
-        t_max = t_mean
+    t_max = reduce_values([t_mean], "max", backend, dev)[0]
     total_bytes = nbytes * (world if prob["scaling"] == "weak" else 1)
     total_flops = flops * (world if prob["scaling"] == "weak" else 1)
     if prob["scaling"] == "strong":
         # config 5: bytes counted per GPU (each replica streams the matrix), summed
-        tb = torch.tensor([nbytes, flops], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tb)
-        total_bytes, total_flops = float(tb[0].item()), float(tb[1].item())
+        total_bytes, total_flops = reduce_values([nbytes, flops], "sum", backend, dev)
     value = total_bytes / t_max / 1e9
 
     # e2e through the C ABI with HOST buffers (pinned), H2D + D2H inside the region
@@ -558,11 +581,7 @@ def run_ours(args):
             for h, out in zip(handles, hx):
                 h.solve_host(z, out)
                 z = out
-        t_e2e = (time.perf_counter() - t0) / k_e2e
-        if world > 1:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = float(tt.item())
+        t_e2e = reduce_values([(time.perf_counter() - t0) / k_e2e], "max", backend, dev)[0]
         e2e = {"value": round(total_bytes / t_e2e / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(hb.numel() * esize * len(handles)),
                "d2h_bytes_per_step": int(hb.numel() * esize * len(handles)),
@@ -737,13 +756,7 @@ def run_blocks(args):
     import workloads
     from paper_1710_04985_b200 import partition
     from paper_1710_04985_b200 import sptrsv as S
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    world, rank, local, dev, backend = init_ranks()
     blocks, p = workloads.config(6)
     owned = partition.factor_assignment([int(b.rowptr[-1]) for b in blocks], world)[rank]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
@@ -792,15 +805,8 @@ def run_blocks(args):
         if world > 1:
             dist.barrier()
     t_mean = float(np.mean([a.elapsed_time(b) for a, b in ev])) / 1e3
-    tb = torch.tensor([t_mean, float(local_bytes), float(local_flops)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = tb[0:1].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tot = tb[1:3].clone()
-        dist.all_reduce(tot)
-        t_max, total_bytes, total_flops = float(tmax.item()), float(tot[0].item()), float(tot[1].item())
-    else:
-        t_max, total_bytes, total_flops = t_mean, float(local_bytes), float(local_flops)
+    t_max = reduce_values([t_mean], "max", backend, dev)[0]
+    total_bytes, total_flops = reduce_values([float(local_bytes), float(local_flops)], "sum", backend, dev)
     # e2e through the C ABI with host buffers
     hb = [it[3].cpu().pin_memory() for it in items]
     hy = [torch.empty_like(v).pin_memory() for v in hb]
@@ -816,11 +822,7 @@ def run_blocks(args):
         for (i, hl, hu, _, _, _), b_, y_, x_ in zip(items, hb, hy, hx):
             hl.solve_host(b_, y_)
             hu.solve_host(y_, x_)
-    t_e2e = (time.perf_counter() - t0) / k_e2e
-    if world > 1:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
+    t_e2e = reduce_values([(time.perf_counter() - t0) / k_e2e], "max", backend, dev)[0]
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
