@@ -38,15 +38,16 @@ void DevArena::release_all() {
     bytes = 0;
 }
 
-// The default memory pool of the device keeps freed memory for reuse (stream-
-// ordered allocations of later handles and temporaries then cost no driver
-// round trip).
+// The default memory pool of the device keeps up to 16 GiB of freed memory
+// for reuse (stream-ordered allocations of later handles and temporaries
+// then cost no driver round trip; beyond that it returns memory at the next
+// synchronisation).
 void keep_pool_memory(int dev) {
     static bool done[64] = {};
     if (dev < 0 || dev >= 64 || done[dev]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
+        uint64_t thr = 16ull << 30;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaGetLastError();
