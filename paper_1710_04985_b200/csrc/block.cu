@@ -137,6 +137,32 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 #ifndef SPTRSV_BLOCK_L2PF
 #define SPTRSV_BLOCK_L2PF 0
 #endif
+// EXT values (shared slots) read at the top of their own step instead of one
+// step ahead: a consumer that has caught up with its producer finds the value
+// landed more often (the LDS overlaps the step's shuffles)
+#ifndef SPTRSV_BLOCK_EXT_LATE
+#define SPTRSV_BLOCK_EXT_LATE 1
+#endif
+// The readiness check of a step's EXT values before its chain (a caught-up
+// consumer spins on the slot and then computes once) instead of after it
+// (speculative chain, redone when a value was late)
+#ifndef SPTRSV_BLOCK_SPIN_FIRST
+#define SPTRSV_BLOCK_SPIN_FIRST 0
+#endif
+// Prologue stagger: a warp whose first row is at level L0 issues its ring
+// prologue max(0, L0 * STAGGER_NS - STAGGER_MARGIN) ns after kernel entry, so
+// the origin tile's first records are not queued behind every warp's (0: off)
+#ifndef SPTRSV_BLOCK_STAGGER_NS
+#define SPTRSV_BLOCK_STAGGER_NS 150
+#endif
+#ifndef SPTRSV_BLOCK_STAGGER_MARGIN
+#define SPTRSV_BLOCK_STAGGER_MARGIN 4000
+#endif
+// The next step's shuffles issued right after this step's value (before its
+// publication stores, whose addresses are computed ahead of the chain)
+#ifndef SPTRSV_BLOCK_EARLY_SHFL
+#define SPTRSV_BLOCK_EARLY_SHFL 1
+#endif
 #ifndef SPTRSV_BLOCK_UB
 #define SPTRSV_BLOCK_UB 4
 #define SPTRSV_BLOCK_DG 16
@@ -475,6 +501,20 @@ __global__ void k_pad_map(int nsteps, const int32_t *step_unit, const int32_t *u
     pmap[s] = pstart[u] + (s - unit_step0[u]);
 }
 
+// level of every warp's first row: the smallest level among the rows of its
+// first non-empty step (0 for a warp without rows)
+__global__ void k_unit_lev0(int U, const int32_t *unit_step0, const unsigned char *ctl, const int32_t *lev,
+                            int32_t *lev0) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= U) return;
+    int best = 0x7fffffff;
+    for (int t = unit_step0[u]; t < unit_step0[u + 1] && best == 0x7fffffff; ++t) {
+        const int4 *c = reinterpret_cast<const int4 *>(ctl + (size_t)t * kCtlBytes);
+        for (int l = 0; l < 32; ++l)
+            if (c[l].w >= 0) best = min(best, lev[c[l].w]);
+    }
+    lev0[u] = best == 0x7fffffff ? 0 : best;
+}
 __global__ void k_pad_count(int U, const int32_t *unit_step0, int32_t *cnt) {
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u < U) cnt[u] = (unit_step0[u + 1] - unit_step0[u] + UNR - 1) / UNR * UNR;
@@ -671,6 +711,7 @@ __device__ __forceinline__ bool is_sent(float v) { return Sentinel<float>::is(v)
 
 struct BlockArgs {
     const int32_t *unit_step0;    // [U+1] padded first step of every warp (multiples of UNR)
+    const int32_t *unit_lev0;     // [U] level of every warp's first row
     const unsigned char *ctl;     // control stream [npad + kPadSteps][kCtlBytes]
     const unsigned char *coef;    // coefficient stream [npad + kPadSteps][Coef<T>::BYTES]
     const int32_t *cta_g0;        // [K+1] mailbox range of every CTA (values it publishes)
@@ -697,6 +738,10 @@ struct Watch {
     unsigned long long t0;
     unsigned it;
     __device__ bool expired(unsigned *status, unsigned long long timeout_ns, unsigned tag) {
+        if (timeout_ns == 0) {               // test hook: give up the first wait
+            st_relaxed(reinterpret_cast<int *>(status), (int)tag);
+            return true;
+        }
         if ((++it & 255u) != 0) return false;
         if (it == 256u) t0 = gtimer();
         if (ld_relaxed(reinterpret_cast<const int *>(status)) == (int)tag) return true;
@@ -855,7 +900,7 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
 #define SPTRSV_BLOCK_FW 4
 #endif
 #ifndef SPTRSV_BLOCK_FSLEEP
-#define SPTRSV_BLOCK_FSLEEP 128
+#define SPTRSV_BLOCK_FSLEEP 0
 #endif
 constexpr int kFw = SPTRSV_BLOCK_FW;
 constexpr unsigned kFsleep = SPTRSV_BLOCK_FSLEEP;      // ns between unproductive poll rounds
@@ -922,6 +967,61 @@ __device__ __forceinline__ void st_remote(uint32_t slots, int r, float v) {
                      slots), "r"(r), "f"(v)
                  : "memory");
 }
+// Publication targets of one step with their addresses computed ahead (off
+// the chain), and the predicated stores that use them right after the step's
+// value is known.
+struct PubA {
+    uint32_t sa, r0, r1;         // shared slot, DSMEM slots of cluster peers (shared::cluster addresses)
+    unsigned ps, p0, p1, pm, px; // predicates (0 / 1)
+    const void *mb;              // mailbox
+    const void *xp;              // x(row)
+};
+template <typename T>
+__device__ __forceinline__ PubA pub_addr(const int4 &pub, int row, uint32_t slots, T *gm, T *x) {
+    PubA P;
+    P.ps = pub.x >= 0;
+    P.sa = slots + (uint32_t)pub.x * (uint32_t)sizeof(T);
+    P.pm = pub.y >= 0;
+    P.mb = gm + (P.pm ? pub.y : 0);
+    P.p0 = pub.z >= 0;
+    P.p1 = pub.w >= 0;
+    const uint32_t a0 = slots + (uint32_t)(pub.z & 0xFFFFFF) * (uint32_t)sizeof(T);
+    const uint32_t a1 = slots + (uint32_t)(pub.w & 0xFFFFFF) * (uint32_t)sizeof(T);
+    const uint32_t k0 = P.p0 ? ((uint32_t)pub.z >> 24) : 0u, k1 = P.p1 ? ((uint32_t)pub.w >> 24) : 0u;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(P.r0) : "r"(a0), "r"(k0));
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(P.r1) : "r"(a1), "r"(k1));
+    P.px = row >= 0;
+    P.xp = x + (P.px ? row : 0);
+    return P;
+}
+__device__ __forceinline__ void pub_store(const PubA &P, double v, bool cl) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cta.f64 [%0], %1;\n\t}"
+                 ::"r"(P.sa), "d"(v), "r"(P.ps) : "memory");
+    if (cl) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cluster.f64 [%0], %1;\n\t}"
+                     ::"r"(P.r0), "d"(v), "r"(P.p0) : "memory");
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cluster.f64 [%0], %1;\n\t}"
+                     ::"r"(P.r1), "d"(v), "r"(P.p1) : "memory");
+    }
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f64 [%0], %1;\n\t}"
+                 ::"l"(P.mb), "d"(v), "r"(P.pm) : "memory");
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f64 [%0], %1;\n\t}"
+                 ::"l"(P.xp), "d"(v), "r"(P.px) : "memory");
+}
+__device__ __forceinline__ void pub_store(const PubA &P, float v, bool cl) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cta.f32 [%0], %1;\n\t}"
+                 ::"r"(P.sa), "f"(v), "r"(P.ps) : "memory");
+    if (cl) {
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cluster.f32 [%0], %1;\n\t}"
+                     ::"r"(P.r0), "f"(v), "r"(P.p0) : "memory");
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.cluster.shared::cluster.f32 [%0], %1;\n\t}"
+                     ::"r"(P.r1), "f"(v), "r"(P.p1) : "memory");
+    }
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.relaxed.gpu.global.f32 [%0], %1;\n\t}"
+                 ::"l"(P.mb), "f"(v), "r"(P.pm) : "memory");
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cg.f32 [%0], %1;\n\t}"
+                 ::"l"(P.xp), "f"(v), "r"(P.px) : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -941,6 +1041,9 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
     constexpr size_t WS = warp_smem_bytes<T>();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int wpc = blockDim.x >> 6;                  // compute warps 0..wpc-1; warp wpc + g fetches for warp g
+#if SPTRSV_BLOCK_TRACE
+    const unsigned long long t_entry = gtimer();      // dev: kernel entry (stored at trace[cap - 2])
+#endif
     unsigned char *ctlring = smem_raw + (size_t)w * WS;                                // [CR][kCtlBytes]
     unsigned char *coefring = ctlring + (size_t)CR * kCtlBytes;                         // [FR][CB]
     T *bland = reinterpret_cast<T *>(coefring + (size_t)FR * CB);                      // [DG][32]
@@ -1029,6 +1132,13 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
         };
 
         // ---- prologue
+        if (SPTRSV_BLOCK_STAGGER_NS > 0) {
+            const long long d = (long long)a.unit_lev0[u] * SPTRSV_BLOCK_STAGGER_NS - SPTRSV_BLOCK_STAGGER_MARGIN;
+            if (d > 0) {
+                const unsigned long long te = gtimer();
+                while (gtimer() - te < (unsigned long long)d) __nanosleep(500);
+            }
+        }
         if (l0)
             for (int kb = 0; kb < min(nbx, DP); ++kb) {
                 l2pf_if(gctl + (size_t)kb * UB * kCtlBytes, UB * kCtlBytes, true);
@@ -1044,11 +1154,16 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
         load_stage(0, S0);
         load_stage(1, S1);
         E3<T> E0;
-        load_ext(S0, E0);
+        if (!SPTRSV_BLOCK_EXT_LATE) load_ext(S0, E0);
         cp_async_wait<DG - 1>();
         T b0 = bland[lane];
         int nrow = ctl_at(DG)->w;               // row of the next far step
         T xprev = T(0);
+        T hc0 = T(0), hc1 = T(0), hc2 = T(0);    // EARLY_SHFL: this step's shuffled values
+#if SPTRSV_BLOCK_TRACE
+        unsigned n_c = 0, n_f = 0, n_p = 0;            // dev: steps that found a ring block / an EXT value late
+        long long cyc_b = 0, cyc_s = 0, cyc_0 = clock64();   // dev: cycles in the b wait / the slow path / total
+#endif
 
         // ---- main loop: UNR steps per iteration.  A step is one basic block:
         // the chain runs speculatively on this step's EXT values while the next
@@ -1067,26 +1182,47 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                     okf = try_coef(kb + 1);
                 }
                 // ---- the chain on this step's values
-                const T h0 = __shfl_sync(0xffffffffu, xprev, S0.c.x);
-                const T h1 = __shfl_sync(0xffffffffu, xprev, S0.c.y);
-                const T h2 = __shfl_sync(0xffffffffu, xprev, S0.c.z);
+                if (SPTRSV_BLOCK_EXT_LATE) load_ext(S0, E0);
+                const T h0 = SPTRSV_BLOCK_EARLY_SHFL ? hc0 : __shfl_sync(0xffffffffu, xprev, S0.c.x);
+                const T h1 = SPTRSV_BLOCK_EARLY_SHFL ? hc1 : __shfl_sync(0xffffffffu, xprev, S0.c.y);
+                const T h2 = SPTRSV_BLOCK_EARLY_SHFL ? hc2 : __shfl_sync(0xffffffffu, xprev, S0.c.z);
+                if (SPTRSV_BLOCK_SPIN_FIRST) {
+                    const unsigned sh0 = sent_hi<T>();
+                    const bool p0 = (hi_word(E0.e0) == sh0) | (hi_word(E0.e1) == sh0) | (hi_word(E0.e2) == sh0);
+                    if (__any_sync(0xffffffffu, p0)) E0 = repoll<T, GL>(E0, S0.c.x, S0.c.y, S0.c.z, &a, tag);
+                }
                 T acc = b0;
                 acc = fnma(S0.f.a0, code_shfl(S0.c.x) ? h0 : E0.e0, acc);
                 acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);
                 acc = fnma(S0.f.a2, code_shfl(S0.c.z) ? h2 : E0.e2, acc);
                 // ---- loads of later steps (independent of the chain)
                 far_load(t + DG, nrow);
+#if SPTRSV_BLOCK_TRACE
+                const long long cw0 = clock64();
                 cp_async_wait<DG - 1>();
+                cyc_b += clock64() - cw0;
+#else
+                cp_async_wait<DG - 1>();
+#endif
                 const T b1 = bland[((t + 1) & (DG - 1)) * 32 + lane];
                 E3<T> E1;
-                load_ext(S1, E1);
+                if (!SPTRSV_BLOCK_EXT_LATE) load_ext(S1, E1);
                 const int nrow1 = ctl_at(t + 1 + DG)->w;
                 Stage<T> S2;
                 load_stage(t + 2, S2);
+                const PubA P = pub_addr<T>(S0.pub, S0.c.w, slots_u32, gm, x);
                 // ---- readiness (value-as-flag; non-EXT terms hold 0) and ring waits
                 const unsigned sh = sent_hi<T>();
                 const bool pend = (hi_word(E0.e0) == sh) | (hi_word(E0.e1) == sh) | (hi_word(E0.e2) == sh);
+#if SPTRSV_BLOCK_TRACE
+                const long long cs0 = clock64();
+#endif
                 if (__any_sync(0xffffffffu, pend || !okc || !okf)) {
+#if SPTRSV_BLOCK_TRACE
+                    n_c += !okc;
+                    n_f += !okf;
+                    n_p += __any_sync(0xffffffffu, pend);
+#endif
                     if (!okc) wait_ctl(t / UB + (DG + UB) / UB);
                     if (!okf) wait_coef(t / UB + 1);
                     if (__any_sync(0xffffffffu, pend)) {
@@ -1098,6 +1234,7 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                     }
                 }
 #if SPTRSV_BLOCK_TRACE
+                cyc_s += clock64() - cs0;
                 if (trc != nullptr && l0 && t < a.trace_cap - 1) trc[t] = gtimer();   // step t's inputs present
 #endif
                 if (OVF) {
@@ -1106,26 +1243,44 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                         acc = ovf_terms<T>(acc, ovf ? S0.c.x - kOvfBase : -1, xprev, &a, tag);
                 }
                 const T xi = UNIT ? Sentinel<T>::scrub(acc) : acc * S0.f.invd;   // a product is never the sentinel
-                st_slot(slots_u32, S0.pub.x, xi);
-                st_mb(gm, S0.pub.y, xi);
+                if (SPTRSV_BLOCK_EARLY_SHFL) {
+                    hc0 = __shfl_sync(0xffffffffu, xi, S1.c.x);
+                    hc1 = __shfl_sync(0xffffffffu, xi, S1.c.y);
+                    hc2 = __shfl_sync(0xffffffffu, xi, S1.c.z);
+                    pub_store(P, xi, CL);
+                } else {
+                    st_slot(slots_u32, S0.pub.x, xi);
+                    st_mb(gm, S0.pub.y, xi);
+                    if (CL) {
+                        st_remote(slots_u32, S0.pub.z, xi);
+                        st_remote(slots_u32, S0.pub.w, xi);
+                    }
+                    st_x(x, S0.c.w, xi);
+                }
 #if SPTRSV_BLOCK_TRACE
                 if (trc != nullptr && a.ptrace != nullptr && S0.pub.y >= 0) a.ptrace[S0.pub.y] = gtimer();
 #endif
-                if (CL) {
-                    st_remote(slots_u32, S0.pub.z, xi);
-                    st_remote(slots_u32, S0.pub.w, xi);
-                }
-                st_x(x, S0.c.w, xi);
                 xprev = xi;
                 S0 = S1;
                 S1 = S2;
-                E0 = E1;
+                if (!SPTRSV_BLOCK_EXT_LATE) E0 = E1;
                 b0 = b1;
                 nrow = nrow1;
             }
         }
         cp_async_wait<0>();
         if (trc != nullptr && l0) trc[a.trace_cap - 1] = gtimer();
+#if SPTRSV_BLOCK_TRACE
+        if (trc != nullptr && l0) {
+            trc[a.trace_cap - 2] = t_entry;
+            trc[a.trace_cap - 3] = n_c;
+            trc[a.trace_cap - 4] = n_f;
+            trc[a.trace_cap - 5] = n_p;
+            trc[a.trace_cap - 6] = cyc_b;
+            trc[a.trace_cap - 7] = cyc_s;
+            trc[a.trace_cap - 8] = clock64() - cyc_0;
+        }
+#endif
     }
     }
 
@@ -1597,6 +1752,9 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
                                              (float *)B.d_ovf_val);
         k_fill_sentinel<float><<<fg, 256, 0, s>>>((float *)B.d_gmb, 2 * (int64_t)std::max(B.G, 4));
     }
+    if ((st = h->arena.alloc_n(&B.d_unit_lev0, (size_t)U)) != SPTRSV_SUCCESS) return st;
+    k_unit_lev0<<<(U + 127) / 128, 128, 0, s>>>(U, B.d_unit_step0, (const unsigned char *)B.d_ctl, h->d_lev,
+                                               B.d_unit_lev0);
     SPTRSV_CUDA(cudaGetLastError());
 
     // ---- launch configuration: K co-resident CTAs of wpc warps
@@ -1639,6 +1797,7 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     if (!B.built) return SPTRSV_ERR_NOT_SUPPORTED;
     BlockArgs a;
     a.unit_step0 = B.d_unit_step0;
+    a.unit_lev0 = B.d_unit_lev0;
     a.ctl = (const unsigned char *)B.d_ctl;
     a.coef = (const unsigned char *)B.d_coef;
     a.cta_g0 = B.d_cta_g0;

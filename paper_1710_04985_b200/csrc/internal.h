@@ -60,6 +60,7 @@ struct BlockPlan {
     size_t smem = 0;
     void *kernel = nullptr;
     int32_t *d_unit_step0 = nullptr;  // [U+1] first step of every warp
+    int32_t *d_unit_lev0 = nullptr;   // [U] level of every warp's first row (prologue stagger)
     void *d_ctl = nullptr;            // step records: control stream (see block.cu)
     void *d_coef = nullptr;           // step records: coefficient stream
     int32_t *d_cta_g0 = nullptr;      // [K+1] mailbox range of every CTA
