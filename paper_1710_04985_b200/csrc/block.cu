@@ -143,12 +143,6 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 #ifndef SPTRSV_BLOCK_EXT_LATE
 #define SPTRSV_BLOCK_EXT_LATE 1
 #endif
-// The readiness check of a step's EXT values before its chain (a caught-up
-// consumer spins on the slot and then computes once) instead of after it
-// (speculative chain, redone when a value was late)
-#ifndef SPTRSV_BLOCK_SPIN_FIRST
-#define SPTRSV_BLOCK_SPIN_FIRST 0
-#endif
 // Prologue stagger: a warp whose first row is at level L0 issues its ring
 // prologue max(0, L0 * STAGGER_NS - STAGGER_MARGIN) ns after kernel entry, so
 // the origin tile's first records are not queued behind every warp's (0: off)
@@ -900,7 +894,7 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
 #define SPTRSV_BLOCK_FW 4
 #endif
 #ifndef SPTRSV_BLOCK_FSLEEP
-#define SPTRSV_BLOCK_FSLEEP 0
+#define SPTRSV_BLOCK_FSLEEP 128
 #endif
 constexpr int kFw = SPTRSV_BLOCK_FW;
 constexpr unsigned kFsleep = SPTRSV_BLOCK_FSLEEP;      // ns between unproductive poll rounds
@@ -1186,11 +1180,6 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
                 const T h0 = SPTRSV_BLOCK_EARLY_SHFL ? hc0 : __shfl_sync(0xffffffffu, xprev, S0.c.x);
                 const T h1 = SPTRSV_BLOCK_EARLY_SHFL ? hc1 : __shfl_sync(0xffffffffu, xprev, S0.c.y);
                 const T h2 = SPTRSV_BLOCK_EARLY_SHFL ? hc2 : __shfl_sync(0xffffffffu, xprev, S0.c.z);
-                if (SPTRSV_BLOCK_SPIN_FIRST) {
-                    const unsigned sh0 = sent_hi<T>();
-                    const bool p0 = (hi_word(E0.e0) == sh0) | (hi_word(E0.e1) == sh0) | (hi_word(E0.e2) == sh0);
-                    if (__any_sync(0xffffffffu, p0)) E0 = repoll<T, GL>(E0, S0.c.x, S0.c.y, S0.c.z, &a, tag);
-                }
                 T acc = b0;
                 acc = fnma(S0.f.a0, code_shfl(S0.c.x) ? h0 : E0.e0, acc);
                 acc = fnma(S0.f.a1, code_shfl(S0.c.y) ? h1 : E0.e1, acc);

@@ -87,3 +87,22 @@ for i in range(len(dt)):
 for a in range(0, nlev, 25):
     seg = hist[a:a + 25]
     print(f"  levels {a:3d}+: mean {seg.mean() * 1e3:5.0f} ns")
+# excess over the fast step, by whether the tile has an input across a cluster / CTA boundary
+cx_ext = tw * 2 * csx                      # cluster extent in x (columns)
+cy_ext = th * 2 * csy
+def kind(u):
+    x0, y0 = TX[u] * tw, TY[u] * th
+    if (x0 % cx_ext == 0 and x0 > 0) or (y0 % cy_ext == 0 and y0 > 0):
+        return "cluster-edge"
+    if (x0 % (2 * tw) == 0 and x0 > 0) or (y0 % (2 * th) == 0 and y0 > 0):
+        return "cta-edge"
+    return "inner" if (x0 > 0 or y0 > 0) else "origin"
+ex = {}
+for i in range(len(dt)):
+    if cross[i + 1]:
+        continue
+    k = kind(path[i + 1][1])
+    e = ex.setdefault(k, [0, 0.0, 0.0])
+    e[0] += 1; e[1] += dt[i]; e[2] += max(0.0, dt[i] - 0.192)
+for k, (c, tot, exc) in ex.items():
+    print(f"  own steps in {k:12s} tiles: {c:3d} steps, {tot:6.1f} us, excess over 192 ns {exc:6.1f} us")
