@@ -170,6 +170,11 @@ constexpr int DG = SPTRSV_BLOCK_DG;    // b(row) loads in flight (steps): cp.asy
 constexpr int UNR = 8;                 // main-loop unroll = per-warp step padding
 constexpr int XB = (DG + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
 constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
+// fetcher warps per compute warp (each polls every kNf-th block of 32 items)
+#ifndef SPTRSV_BLOCK_NF
+#define SPTRSV_BLOCK_NF 2
+#endif
+constexpr int kNf = SPTRSV_BLOCK_NF;
 constexpr int kZeroSlots = 64;         // shared slots 0..63 hold 0.0: the EXT read of a non-EXT term
 static_assert(NCB > DC && NFB > DF && DG % UNR == 0 && UNR % UB == 0, "ring shapes");
 static_assert((DG + 1 + UB - 1) / UB + 2 <= DC, "control records must land before their b gather");
@@ -833,7 +838,7 @@ template <typename T> struct E3 { T e0, e1, e2; };
 template <typename T, bool GL>
 __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const BlockArgs *pa, unsigned tag) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int wpc = blockDim.x >> 6;
+    const int wpc = blockDim.x / (32 * (1 + kNf));
     const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
     const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
     Watch wd{0, 0};
@@ -855,7 +860,7 @@ __device__ __noinline__ E3<T> repoll(E3<T> e, int c0, int c1, int c2, const Bloc
 template <typename T>
 __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, unsigned tag) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int wpc = blockDim.x >> 6;
+    const int wpc = blockDim.x / (32 * (1 + kNf));
     const T *slots = reinterpret_cast<const T *>(smem_raw + (size_t)wpc * warp_smem_bytes<T>());
     const T *gm = static_cast<const T *>(pa->gmb) + (size_t)((tag - 1u) & 1u) * pa->G;
     const int32_t *oc = pa->ovf_code;
@@ -891,7 +896,7 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
 #define SPTRSV_BLOCK_RSLEEP 0
 #endif
 #ifndef SPTRSV_BLOCK_FW
-#define SPTRSV_BLOCK_FW 4
+#define SPTRSV_BLOCK_FW 1
 #endif
 #ifndef SPTRSV_BLOCK_FSLEEP
 #define SPTRSV_BLOCK_FSLEEP 128
@@ -900,17 +905,17 @@ constexpr int kFw = SPTRSV_BLOCK_FW;
 constexpr unsigned kFsleep = SPTRSV_BLOCK_FSLEEP;      // ns between unproductive poll rounds
 template <typename T>
 __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
-                        unsigned long long tmo, unsigned tag, unsigned long long *ftrace) {
+                        unsigned long long tmo, unsigned tag, unsigned long long *ftrace, int part) {
     const int lane = threadIdx.x & 31;
     Watch wd{0, 0};
     int2 d[kFw];
     int id[kFw];
-    int nxt = f0 + lane;                      // next item of this lane
+    int nxt = f0 + 32 * part + lane;          // next item of this lane (fetcher part of kNf: items in blocks of 32)
 #pragma unroll
     for (int k = 0; k < kFw; ++k) {
         d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
         id[k] = nxt;
-        nxt += 32;
+        nxt += 32 * kNf;
     }
     for (;;) {
         bool live = false;
@@ -928,7 +933,7 @@ __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots
                 if (ftrace != nullptr) ftrace[id[k]] = gtimer();
                 d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
                 id[k] = nxt;
-                nxt += 32;
+                nxt += 32 * kNf;
                 got = true;
             }
         if (!__any_sync(0xffffffffu, got)) {      // nothing arrived: back off (polls load L2 for everyone)
@@ -1026,7 +1031,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 // through the CTA's fetcher warp and a shared slot.  The common instance
 // (no OVF, no GL) carries no code for either.
 template <typename T, bool UNIT, bool OVF, bool GL, bool CL>
-__global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockArgs a) {
+__global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_constant__ BlockArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ unsigned s_epoch;
     constexpr int CB = Coef<T>::BYTES;
@@ -1034,7 +1039,7 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
     static_assert((CR & (CR - 1)) == 0 && (FR & (FR - 1)) == 0, "power-of-two rings");
     constexpr size_t WS = warp_smem_bytes<T>();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int wpc = blockDim.x >> 6;                  // compute warps 0..wpc-1; warp wpc + g fetches for warp g
+    const int wpc = blockDim.x / (32 * (1 + kNf));   // compute warps 0..wpc-1; warps wpc + g + wpc p fetch for warp g
 #if SPTRSV_BLOCK_TRACE
     const unsigned long long t_entry = gtimer();      // dev: kernel entry (stored at trace[cap - 2])
 #endif
@@ -1066,9 +1071,9 @@ __global__ void __launch_bounds__(256, 1) k_block(const __grid_constant__ BlockA
     }
 
     if (w >= wpc) {
-        const int fu = blockIdx.x * wpc + (w - wpc);      // the compute warp whose items this warp fetches
+        const int fu = blockIdx.x * wpc + (w - wpc) % wpc;   // the compute warp whose items this warp fetches
         if (!GL) fetcher<T>(a.fitems, a.fptr[fu], a.fptr[fu + 1], gm, slots, a.status, a.timeout_ns, tag,
-                          a.ftrace);
+                          a.ftrace, (w - wpc) / wpc);
     } else {
     const int u = blockIdx.x * wpc + w;
     const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;    // n: a multiple of UNR
@@ -1499,7 +1504,7 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
             static const int cshapes[][2] = {{2, 4}, {4, 2}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}};
             for (auto &c : cshapes) {
                 if (cxn % c[0] || cyn % c[1]) continue;
-                if (!clusters_fit(h, f64, c[0] * c[1], K, 64 * wpc, budget)) continue;
+                if (!clusters_fit(h, f64, c[0] * c[1], K, 32 * (1 + kNf) * wpc, budget)) continue;
                 csx = c[0];
                 csy = c[1];
                 break;
@@ -1752,11 +1757,11 @@ sptrsv_status_t block_build(sptrsv_handle_t h, cudaStream_t s) {
     const size_t smem = fixed + (size_t)B.nslots * es;
     SPTRSV_CUDA(cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 64 * wpc, smem));
+    SPTRSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kn, 32 * (1 + kNf) * wpc, smem));
     if (per_sm * h->num_sms < K) return SPTRSV_ERR_NOT_SUPPORTED;
     B.kernel = kn;
     B.smem = smem;
-    B.threads = 64 * wpc;                // wpc compute warps + one fetcher warp each
+    B.threads = 32 * (1 + kNf) * wpc;    // wpc compute warps + kNf fetcher warps each
     B.rec_bytes = kCtlBytes + CB;
     B.nent = (int64_t)npad * (kCtlBytes + CB);
     SPTRSV_CUDA(cudaStreamSynchronize(s));
