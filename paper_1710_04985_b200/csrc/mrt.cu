@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                 gave_up = __any_sync(0xffffffffu, gave_up);
             }
             // acquire: the producers' x rows are visible, then also to the async proxy
-            asm volatile("fence.acquire.gpu;\n\tfence.proxy.async.global;" ::: "memory");
             const int h0 = a.hptr[g], nh = a.hptr[g + 1] - h0;
+            // the proxy fence only where TMA reads follow (a group without halo rows skips it)
+            if (nh > 0) asm volatile("fence.acquire.gpu;\n\tfence.proxy.async.global;" ::: "memory");
+            else asm volatile("fence.acquire.gpu;" ::: "memory");
             uint64_t *hb = &mbar[3 + (k & 1)];
             if (lane == 0) mbar_arrive_expect_tx(hb, (uint32_t)nh * rowbytes);
             __syncwarp();
