@@ -175,6 +175,7 @@ constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
 #define SPTRSV_BLOCK_NF 2
 #endif
 constexpr int kNf = SPTRSV_BLOCK_NF;
+
 constexpr int kZeroSlots = 64;         // shared slots 0..63 hold 0.0: the EXT read of a non-EXT term
 static_assert(NCB > DC && NFB > DF && DG % UNR == 0 && UNR % UB == 0, "ring shapes");
 static_assert((DG + 1 + UB - 1) / UB + 2 <= DC, "control records must land before their b gather");
