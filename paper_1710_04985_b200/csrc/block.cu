@@ -157,6 +157,11 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 #ifndef SPTRSV_BLOCK_EARLY_SHFL
 #define SPTRSV_BLOCK_EARLY_SHFL 1
 #endif
+// the idle mailbox array re-armed at the end of a solve (for the next one)
+// instead of at its start (where the stores meet every warp's prologue)
+#ifndef SPTRSV_BLOCK_REARM_END
+#define SPTRSV_BLOCK_REARM_END 1
+#endif
 #ifndef SPTRSV_BLOCK_UB
 #define SPTRSV_BLOCK_UB 4
 #define SPTRSV_BLOCK_DG 16
@@ -1065,7 +1070,7 @@ __global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_const
     const unsigned epoch = s_epoch;
     const unsigned tag = epoch + 1u;
     T *gm = static_cast<T *>(a.gmb) + (size_t)(epoch & 1u) * a.G;
-    {   // re-arm this CTA's mailboxes of the idle array (written by the previous solve)
+    if (!SPTRSV_BLOCK_REARM_END) {   // re-arm this CTA's mailboxes of the idle array (written by the previous solve)
         T *go = static_cast<T *>(a.gmb) + (size_t)((epoch & 1u) ^ 1u) * a.G;
         for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
             go[i] = Sentinel<T>::value();
@@ -1279,6 +1284,11 @@ __global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_const
     }
     }
 
+    if (SPTRSV_BLOCK_REARM_END) {    // re-arm this CTA's mailboxes of the idle array for the next solve
+        T *go = static_cast<T *>(a.gmb) + (size_t)((epoch & 1u) ^ 1u) * a.G;
+        for (int i = a.cta_g0[blockIdx.x] + threadIdx.x; i < a.cta_g0[blockIdx.x + 1]; i += blockDim.x)
+            go[i] = Sentinel<T>::value();
+    }
     if (CL) cluster_sync_all();      // no CTA leaves while a cluster peer may still store into it
     else __syncthreads();
     if (threadIdx.x == 0) {      // the last CTA to finish advances the mailbox epoch
