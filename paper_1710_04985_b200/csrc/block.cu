@@ -172,7 +172,10 @@ constexpr int NCB = 8, DC = 7;         // control ring (blocks) / TMA lookahead 
 constexpr int NFB = 4, DF = 3;         // coefficient ring (blocks) / TMA lookahead (blocks)
 constexpr int DP = SPTRSV_BLOCK_DP;    // L2 prefetch lookahead (blocks), both streams
 constexpr int DG = SPTRSV_BLOCK_DG;    // b(row) loads in flight (steps): cp.async landing ring
-constexpr int UNR = 8;                 // main-loop unroll = per-warp step padding
+#ifndef SPTRSV_BLOCK_UNR
+#define SPTRSV_BLOCK_UNR 8
+#endif
+constexpr int UNR = SPTRSV_BLOCK_UNR;   // main-loop unroll = per-warp step padding
 constexpr int XB = (DG + 1) / UB + 2;  // blocks staged past a warp's last step (lookahead)
 constexpr int kPadSteps = (XB + 1) * UB;   // stream padding past the last warp
 // fetcher warps per compute warp (each polls every kNf-th block of 32 items)
