@@ -33,14 +33,16 @@
 // kernel, so results are run-to-run bitwise reproducible and equal across
 // algorithms that share it (reading Q8).
 //
-// One warp per tile does everything; nothing on its per-step critical chain
-// (shuffle -> select -> 3 FMA -> multiply) waits on memory:
-//   records   (codes, coefficients, publish slots) of step t+DR*UB: TMA bulk
-//             copies into a per-warp ring (no L2 prefetch: see SPTRSV_BLOCK_L2PF)
-//   row ids   TMA into a per-warp ring DW blocks ahead
-//   b(row)    cp.async gathers into a per-warp ring DBS steps ahead
-//   GLOB EXT  relaxed loads DG steps ahead into a register ring
-//   SMEM EXT  volatile shared loads one step ahead
+// One compute warp per tile; nothing on its per-step critical chain
+// (shuffle -> select -> 3 FMA -> multiply) waits on global memory:
+//   records   (codes, row ids, coefficients, publication targets): TMA bulk
+//             copies into per-warp rings DC / DF blocks ahead (no L2 prefetch:
+//             see SPTRSV_BLOCK_L2PF)
+//   b(row)    cp.async gathers into a per-warp ring DG steps ahead
+//   EXT       values of other warps / CTAs: shared-slot loads at the top of
+//             the step (cluster peers store into them over DSMEM; values from
+//             other clusters are copied in by kNf fetcher warps per compute
+//             warp, which poll the global mailboxes)
 // A value still holding the sentinel when its step comes is re-polled (the
 // only wait).  A per-solve watchdog (timeout_ns) turns a hung wait into
 // SPTRSV_ERR_TIMEOUT via sptrsv_get_solve_status instead of a hung GPU.
@@ -120,8 +122,10 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 // per step, so `cp.async.wait_group DG-1` waits for exactly the oldest step's
 // load (register-ring loads would share counting scoreboards and wait for the
 // newest ones too).  Values from other CTAs reach shared slots through the
-// CTA's fetcher warp, so a step only reads shared memory, every load one step
-// before its use (stage registers).  SHFL and NONE codes (< 32, 32) address
+// fetcher warps or DSMEM stores, so a step only reads shared memory: records
+// two steps ahead (stage registers), EXT slots at the top of the step.  The
+// next step's shuffles are issued right after a step's value, before its
+// publication stores (whose addresses are computed ahead).  SHFL and NONE codes (< 32, 32) address
 // the zero slots, so the EXT read of every term is one unconditional LDS.
 // Per-step / publication timestamps (tools/block_trace2.py, crit_path.py) are
 // compiled only into development builds: python tools/build_variant.py trace
@@ -896,11 +900,14 @@ __device__ __noinline__ T ovf_terms(T acc, int o, T xprev, const BlockArgs *pa, 
     return acc;
 }
 
-// The fetcher (last warp of a CTA): copies the CTA's inbound values (written
-// to global mailboxes by other CTAs) into their shared slots, in the order
-// the CTA's steps need them.  Lane l owns items l, l+32, ...; it keeps kFw of
-// them polled at once (relaxed loads) and refills each window entry as soon
-// as its value arrived (no head-of-line blocking).
+// The fetchers (kNf warps per compute warp): copy the warp's inbound values
+// (written to global mailboxes by CTAs of other clusters) into their shared
+// slots, in the order the warp's steps need them.  Fetcher p, lane l owns the
+// items 32 p + l + 32 kNf j; it keeps kFw of them polled at once (relaxed
+// loads) and refills each window entry as soon as its value arrived (no
+// head-of-line blocking).  Two fetchers with one item per lane measured best
+// (cfg2 118 vs 130 us with one fetcher of four: a refill then waits for one
+// item-list load, not for a round of four polls).
 #ifndef SPTRSV_BLOCK_RSLEEP
 #define SPTRSV_BLOCK_RSLEEP 0
 #endif
