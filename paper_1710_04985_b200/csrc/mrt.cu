@@ -46,7 +46,15 @@ namespace {
 constexpr int kGmax = 128;                         // rows per group
 constexpr int kHmax = 32;                          // halo rows per group
 constexpr int kCw = 16;                            // compute warps per CTA
-constexpr int kThreadsMrt = (kCw + 1) * 32;        // + the loader warp
+// a release warp publishes the CTA's progress after each group barrier (the
+// st.release waits ~1 us for the group's x stores to drain) while the loader
+// warp already waits for the next group's producers and copies its halo
+#ifndef SPTRSV_MRT_RELW
+#define SPTRSV_MRT_RELW 1
+#endif
+constexpr int kRelw = SPTRSV_MRT_RELW;
+
+constexpr int kThreadsMrt = (kCw + 1 + kRelw) * 32;        // + the loader warp (+ the release warp)
 constexpr int kRpw = kGmax / kCw;                  // rows per compute warp per group
 constexpr int kMaxDeps = 4;
 constexpr int kCols = 64;                          // columns per launch (column blocks of <= 64)
@@ -130,6 +138,14 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     T *x = static_cast<T *>(a.x);
     const uint32_t rowbytes = (uint32_t)a.ncols * (uint32_t)sizeof(T);
 
+    if (kRelw && w == kCw + 1) {
+        // ---- release warp: progress counter after every group barrier
+        for (int k = 0; k <= ng; ++k) {
+            bar_all();
+            if (lane == 0 && k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
+        }
+        return;
+    }
     if (w == kCw) {
         // ---- loader warp: records, producer waits, halo copies, progress releases
         auto issue_meta = [&](int k) {
@@ -144,12 +160,31 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
         bool gave_up = false;
         unsigned long long *tr = a.trace != nullptr ? a.trace + (size_t)c * a.trace_cap * 2 : nullptr;
         // waits for group k's producers, then copies its halo rows by TMA (mbar[3 + (k & 1)])
-        auto prepare = [&](int k) {
-            if (k >= ng) return;
+        // a group's wait and halo lists, loaded one group ahead (lane e holds wait
+        // entry e < 32 and halo row e < kHmax): their global-load latency stays
+        // off the loader's chain
+        struct Meta {
+            int w0, w1, h0, nh, hr;
+            int2 wt;
+        };
+        auto load_meta = [&](int k) -> Meta {
+            Meta m{0, 0, 0, 0, 0, make_int2(0, 0)};
+            if (k >= ng) return m;
             const int g = g0 + k;
+            m.w0 = a.wptr[g];
+            m.w1 = a.wptr[g + 1];
+            m.h0 = a.hptr[g];
+            m.nh = a.hptr[g + 1] - m.h0;
+            if (m.w0 + lane < m.w1) m.wt = a.waits[m.w0 + lane];
+            if (lane < m.nh) m.hr = a.hrow[m.h0 + lane];
+            return m;
+        };
+        // waits for group k's producers, then copies its halo rows by TMA (mbar[3 + (k & 1)])
+        auto prepare = [&](int k, const Meta &m) {
+            if (k >= ng) return;
             if (!gave_up) {
-                for (int e = a.wptr[g] + lane; e < a.wptr[g + 1]; e += 32) {
-                    const int2 wt = a.waits[e];
+                for (int e = m.w0 + lane; e < m.w1; e += 32) {
+                    const int2 wt = e - m.w0 < 32 ? m.wt : a.waits[e];
                     const unsigned long long target = ep | (unsigned)wt.y;
                     unsigned it = 0;
                     unsigned long long t0 = 0;
@@ -168,30 +203,33 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                 gave_up = __any_sync(0xffffffffu, gave_up);
             }
             // acquire: the producers' x rows are visible, then also to the async proxy
-            const int h0 = a.hptr[g], nh = a.hptr[g + 1] - h0;
-            // the proxy fence only where TMA reads follow (a group without halo rows skips it)
+            // (the proxy fence only where TMA reads follow)
+            const int nh = m.nh;
             if (nh > 0) asm volatile("fence.acquire.gpu;\n\tfence.proxy.async.global;" ::: "memory");
             else asm volatile("fence.acquire.gpu;" ::: "memory");
             uint64_t *hb = &mbar[3 + (k & 1)];
-            if (lane == 0) mbar_arrive_expect_tx(hb, (uint32_t)nh * rowbytes);
-            __syncwarp();
             const uint32_t hd = halo_of(k);
-            for (int h = lane; h < nh; h += 32)
-                bulk_g2s_u32(hd + (uint32_t)h * RS, x + (int64_t)a.hrow[h0 + h] * a.ld, rowbytes, hb);
+            {
+                if (lane == 0) mbar_arrive_expect_tx(hb, (uint32_t)nh * rowbytes);
+                __syncwarp();
+                if (lane < nh) bulk_g2s_u32(hd + (uint32_t)lane * RS, x + (int64_t)m.hr * a.ld, rowbytes, hb);
+            }
         };
         if (lane == 0) {
             issue_meta(0);
             issue_meta(1);
         }
-        prepare(0);
+        Meta mn = load_meta(1);
+        prepare(0, load_meta(0));
         for (int k = 0; k <= ng; ++k) {
             bar_all();                          // barrier k: group k-1 done, group k's halo issued
             if (tr != nullptr && lane == 0 && k < a.trace_cap) tr[2 * k] = gtime();
             if (lane == 0) {
-                if (k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
+                if (!kRelw && k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
                 issue_meta(k + 2);              // its ring slot held group k-1's records
             }
-            prepare(k + 1);                     // overlaps group k
+            prepare(k + 1, mn);                 // overlaps group k
+            mn = load_meta(k + 2);
             if (tr != nullptr && lane == 0 && k < a.trace_cap) tr[2 * k + 1] = gtime();
         }
         return;
