@@ -37,7 +37,7 @@ def _compile(cu: str, headers_mtime: float, force: bool, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.basename(cu)[:-3] + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(cu), headers_mtime):
         return obj
-    tmp = obj + f".tmp{os.getpid()}"
+    tmp = obj + ".tmp.o"          # a fixed name: the build is reproducible (same bytes, same sha256)
     cmd = [nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-c", "-o", tmp, cu]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
@@ -55,11 +55,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     hdr = max(os.path.getmtime(s) for s in srcs if not s.endswith(".cu"))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(cu))) as ex:
         objs = list(ex.map(lambda c: _compile(c, hdr, force, verbose), cu))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = LIB + ".tmp.so"
     cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    # the host objects name nvcc's per-process temporary files (tmpxft_<pid>_...)
+    # in their local symbol table; without it the library is byte-for-byte
+    # reproducible, so its sha256 identifies the build (profiles/ncu_traffic.json)
+    try:
+        subprocess.check_call(["strip", "--strip-unneeded", tmp])
+    except (OSError, subprocess.CalledProcessError):
+        pass
     os.replace(tmp, LIB)
     return LIB
 
