@@ -1,4 +1,4 @@
-"""Context baselines for bench.py (not the product): cuSPARSE SpSV."""
+"""Context baselines for bench.py (not the product): cuSPARSE SpSV and SpSM."""
 from __future__ import annotations
 
 import ctypes
@@ -37,6 +37,14 @@ def _load():
         lib.spsv_solve.argtypes = [vp, vp]
         lib.spsv_destroy.restype = None
         lib.spsv_destroy.argtypes = [vp]
+        lib.spsm_create.restype = ctypes.c_int
+        lib.spsm_create.argtypes = [ctypes.c_int, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, ctypes.c_int, vp, vp, ctypes.POINTER(vp),
+                                    ctypes.POINTER(ctypes.c_float)]
+        lib.spsm_solve.restype = ctypes.c_int
+        lib.spsm_solve.argtypes = [vp, vp]
+        lib.spsm_destroy.restype = None
+        lib.spsm_destroy.argtypes = [vp]
         _lib = lib
     return _lib
 
@@ -81,5 +89,36 @@ class CusparseSpSV:
     def __del__(self):
         try:
             _load().spsv_destroy(self.ctx)
+        except Exception:
+            pass
+
+
+class CusparseSpSM:
+    """cuSPARSE SpSM on one triangle: X = T^{-1} B, B / X row-major (n, nrhs) torch CUDA tensors."""
+
+    def __init__(self, m, uplo, diag, b, x, dtype=np.float64):
+        import torch
+        rp, ci, va = triangle(m, uplo, keep_diag=True)
+        self._keep = [torch.from_numpy(rp).cuda(), torch.from_numpy(ci).cuda(),
+                      torch.from_numpy(va.astype(dtype)).cuda(), b, x]
+        out = ctypes.c_void_p()
+        an = ctypes.c_float(0.0)
+        st = _load().spsm_create(m.n, int(ci.size), self._keep[0].data_ptr(), self._keep[1].data_ptr(),
+                                 self._keep[2].data_ptr(), int(uplo == "upper"), int(diag == "unit"),
+                                 int(dtype == np.float32), int(b.shape[1]), b.data_ptr(), x.data_ptr(),
+                                 ctypes.byref(out), ctypes.byref(an))
+        self.analysis_ms = float(an.value)      # cusparseSpSM_analysis alone (CUDA events)
+        if st != 0:
+            raise RuntimeError(f"cuSPARSE SpSM setup failed ({st})")
+        self.ctx = out
+
+    def solve(self, stream_ptr: int):
+        st = _load().spsm_solve(self.ctx, ctypes.c_void_p(stream_ptr))
+        if st != 0:
+            raise RuntimeError(f"cuSPARSE SpSM solve failed ({st})")
+
+    def __del__(self):
+        try:
+            _load().spsm_destroy(self.ctx)
         except Exception:
             pass

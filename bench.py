@@ -589,7 +589,7 @@ def run_ours(args):
 
     # cuSPARSE SpSV on the same problem, same protocol (context)
     cusp = None
-    if not args.no_cusparse and world == 1 and nrhs == 1:
+    if not args.no_cusparse and world == 1:
         try:
             import baseline
             npdt = np.float64 if args.dtype == "f64" else np.float32
@@ -602,8 +602,9 @@ def run_ours(args):
             ctxs, z = [], b
             torch.cuda.synchronize()
             t_ca = time.perf_counter()
+            Cls = baseline.CusparseSpSV if nrhs == 1 else baseline.CusparseSpSM     # SpSM for cfg5
             for (uplo, diag), out in zip(solves, cbufs):
-                ctxs.append(baseline.CusparseSpSV(m, uplo, diag, z, out, npdt))
+                ctxs.append(Cls(m, uplo, diag, z, out, npdt))
                 z = out
             torch.cuda.synchronize()
             cusp_an_ms = sum(c.analysis_ms for c in ctxs)        # cusparseSpSV_analysis, CUDA events
@@ -630,8 +631,10 @@ def run_ours(args):
                     "speedup_ours": round(tc / t_mean, 3), "max_rel_diff_vs_ours": diff,
                     "analysis_ms": round(cusp_an_ms, 2),
                     "break_even_solves_vs_ours": break_even_solves(analysis_ms * 1e-3, t_mean, cusp_an_ms * 1e-3, tc),
-                    "analysis_note": "cusparseSpSV_analysis only (CUDA events); ours: wall clock of sptrsv_analyze + set_algo builds on device-resident CSR, warm process; break_even_solves_vs_ours = Table 7's n_s (P:1412-1420), null if none",
-                    "api": "cusparseSpSV_solve (CUSPARSE_SPSV_ALG_DEFAULT), analysis outside the timing"}
+                    "analysis_note": "cusparseSpSV_analysis / cusparseSpSM_analysis only (CUDA events); ours: wall clock of sptrsv_analyze + set_algo builds on device-resident CSR, warm process; break_even_solves_vs_ours = Table 7's n_s (P:1412-1420), null if none",
+                    "api": ("cusparseSpSV_solve (CUSPARSE_SPSV_ALG_DEFAULT)" if nrhs == 1 else
+                            f"cusparseSpSM_solve (CUSPARSE_SPSM_ALG_DEFAULT, {nrhs} row-major RHS)")
+                           + ", analysis outside the timing"}
             del ctxs
         except Exception as e:              # context only: never fails the bench
             cusp = {"unavailable": str(e)[:200]}
