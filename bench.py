@@ -174,6 +174,15 @@ def break_even_solves(setup_ours, solve_ours, setup_other, solve_other):
     return max(n, 1)
 
 
+def build_digest():
+    """sha256 of the library's sources and nvcc flags (build.source_digest)."""
+    from paper_1710_04985_b200 import build as B
+    try:
+        return B.source_digest()
+    except OSError:
+        return None
+
+
 def lib_sha256():
     import hashlib
     from paper_1710_04985_b200 import build as B
@@ -209,15 +218,15 @@ def measured_peak():
 def ncu_traffic(key, sha):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel, from an ncu --set full capture of THIS library build (entries are
-    keyed by config/kernel/dtype and carry the sha256 of libsptrsv.so they were
-    measured on; any other build -> None)."""
+    keyed by config/kernel/dtype and carry the build digest -- sha256 of the
+    sources and nvcc flags -- they were measured on; any other build -> None)."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             ent = json.load(f).get(key)
     except Exception:
         return None
-    if not isinstance(ent, dict) or sha is None or ent.get("lib_sha256") != sha:
+    if not isinstance(ent, dict) or sha is None or ent.get("build_digest") != sha:
         return None
     return ent.get("bytes")
 
@@ -700,7 +709,7 @@ def run_ours(args):
         t_lev, lev_probe = None, {"unavailable": str(e)[:120]}
     eff_algo = "+".join(sorted({ALGO_NAMES.get(i["algo"], "?") for i in an_infos}))
     key = f"cfg{args.config}_{kinfo[dom][0]}_{args.dtype}"
-    sha = lib_sha256()
+    sha = build_digest()
     clk_s = clk.summary()
     line = {
         "metric": "SpTRSV effective HBM GB/s per solve (fraction of B200 peak)",
@@ -719,7 +728,7 @@ def run_ours(args):
                    "parallelism": f"replicas{world}" if prob["scaling"] == "weak" else f"rhs-partition{world}"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": ncu_traffic(key, sha), "peak_source": peak_src,
-                     "traffic_source": "profiles/ncu_traffic.json entry of this libsptrsv.so build (sha256), else null",
+                     "traffic_source": "profiles/ncu_traffic.json entry of this build (sha256 of its sources and nvcc flags), else null",
                      "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
                      "kernel": kinfo[dom][0], "kernel_us": round(t_dom * 1e6, 2),
                      "bytes_per_launch": int(per_solve[dom][0]),
@@ -730,7 +739,7 @@ def run_ours(args):
                      "latency_floor_probe": lev_probe,
                      "ns_per_level_achieved": round(t_dom * 1e9 / max(1, an_infos[dom]["nlev"]), 1)},
         "parity": parity,
-        "lib_sha256": sha,
+        "build_digest": sha, "lib_sha256": lib_sha256(),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(args.steps * launches_per_step),

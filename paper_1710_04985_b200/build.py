@@ -28,6 +28,21 @@ def sources():
                   + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "sptrsv.h")])
 
 
+def source_digest() -> str:
+    """sha256 over the nvcc flags and the sources (paths relative to the repo,
+    contents): identifies a build independently of file times (the -lineinfo
+    tables embed source mtimes, so the library bytes differ between builds of
+    the same sources).  profiles/ncu_traffic.json entries are keyed by it."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(" ".join(NVCC_FLAGS + ARCH).encode())
+    for src in sources():
+        h.update(os.path.relpath(src, ROOT).encode() + b"\0")
+        with open(src, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def nvcc() -> str:
     cand = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     return cand if os.path.exists(cand) else "nvcc"
@@ -37,7 +52,7 @@ def _compile(cu: str, headers_mtime: float, force: bool, verbose: bool) -> str:
     obj = os.path.join(OBJDIR, os.path.basename(cu)[:-3] + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(cu), headers_mtime):
         return obj
-    tmp = obj + ".tmp.o"          # a fixed name: the build is reproducible (same bytes, same sha256)
+    tmp = obj + ".tmp.o"          # a fixed name (nvcc records the output path)
     cmd = [nvcc(), *NVCC_FLAGS, "-I" + INCLUDE, "-I" + CSRC, "-c", "-o", tmp, cu]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
@@ -61,8 +76,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
     # the host objects name nvcc's per-process temporary files (tmpxft_<pid>_...)
-    # in their local symbol table; without it the library is byte-for-byte
-    # reproducible, so its sha256 identifies the build (profiles/ncu_traffic.json)
+    # in their local symbol table (not needed: ctypes binds the dynamic symbols).
+    # The library bytes still depend on the sources' mtimes (-lineinfo);
+    # source_digest() identifies a build
     try:
         subprocess.check_call(["strip", "--strip-unneeded", tmp])
     except (OSError, subprocess.CalledProcessError):

@@ -1,7 +1,8 @@
 """Record the DRAM traffic per launch of a kernel from an ncu --set full
-report into profiles/ncu_traffic.json, tagged with the sha256 of the
-libsptrsv.so build the report was taken on (bench.py only uses an entry whose
-sha matches the library it runs).
+report into profiles/ncu_traffic.json, tagged with the build digest (sha256 of
+the library's sources and nvcc flags, build.source_digest) of the build the
+report was taken on (bench.py only uses an entry whose digest matches the
+library it runs).
 
 python tools/ncu_traffic.py REPORT.ncu-rep KEY [KERNEL_REGEX]
   KEY e.g. cfg2_k_block_f64 (cfg<config>_<kernel>_<dtype>, as bench.py builds it)
@@ -34,7 +35,10 @@ def main():
                         float(r[wr].replace(",", "")) * scale.get(units[wr], 1))
     if not vals:
         sys.exit(f"no launch of {pat.pattern} in {rep}")
-    with open(os.path.join(ROOT, "paper_1710_04985_b200", "lib", "libsptrsv.so"), "rb") as f:
+    sys.path.insert(0, ROOT)
+    from paper_1710_04985_b200 import build as B
+    digest = B.source_digest()
+    with open(B.LIB, "rb") as f:
         sha = hashlib.sha256(f.read()).hexdigest()
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -43,7 +47,7 @@ def main():
     except (OSError, ValueError):
         db = {}
     db = {k: v for k, v in db.items() if isinstance(v, dict)}      # drop round-1 unversioned entries
-    db[key] = {"bytes": int(sum(vals) / len(vals)), "launches": len(vals), "lib_sha256": sha,
+    db[key] = {"bytes": int(sum(vals) / len(vals)), "launches": len(vals), "build_digest": digest, "lib_sha256": sha,
                "source": f"ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum, {os.path.basename(rep)}"}
     with open(path, "w") as f:
         json.dump(db, f, indent=1, sort_keys=True)
