@@ -166,6 +166,21 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 #ifndef SPTRSV_BLOCK_REARM_END
 #define SPTRSV_BLOCK_REARM_END 1
 #endif
+// Development builds with bounds checks of every record-driven index (shared
+// slot, mailbox, cluster rank, row): a violation prints and traps.  Stands in
+// for compute-sanitizer where the tool is not available
+// (python tools/build_variant.py check -DSPTRSV_BLOCK_CHECK=1).
+#ifndef SPTRSV_BLOCK_CHECK
+#define SPTRSV_BLOCK_CHECK 0
+#endif
+#define SPTRSV_BCHECK(cond, what, v)                                                                             \
+    do {                                                                                                         \
+        if (SPTRSV_BLOCK_CHECK && !(cond)) {                                                                     \
+            printf("k_block bounds check failed: %s = %d (block %d thread %d)\n", what, (int)(v), blockIdx.x,  \
+                   threadIdx.x);                                                                                \
+            __trap();                                                                                            \
+        }                                                                                                        \
+    } while (0)
 #ifndef SPTRSV_BLOCK_UB
 #define SPTRSV_BLOCK_UB 4
 #define SPTRSV_BLOCK_DG 16
@@ -741,6 +756,7 @@ struct BlockArgs {
     const void *b;
     void *x;
     int G, nslots;                // nslots: shared slots per CTA including the kZeroSlots
+    int n, cs;                    // rows, CTAs per cluster (bounds checks of development builds)
     unsigned long long timeout_ns;
 };
 
@@ -921,7 +937,8 @@ constexpr int kFw = SPTRSV_BLOCK_FW;
 constexpr unsigned kFsleep = SPTRSV_BLOCK_FSLEEP;      // ns between unproductive poll rounds
 template <typename T>
 __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots, unsigned *status,
-                        unsigned long long tmo, unsigned tag, unsigned long long *ftrace, int part) {
+                        unsigned long long tmo, unsigned tag, unsigned long long *ftrace, int part, int G,
+                        int nslots) {
     const int lane = threadIdx.x & 31;
     Watch wd{0, 0};
     int2 d[kFw];
@@ -945,6 +962,7 @@ __device__ void fetcher(const int2 *items, int f0, int f1, const T *gm, T *slots
 #pragma unroll
         for (int k = 0; k < kFw; ++k)
             if (d[k].x >= 0 && !is_sent(v[k])) {
+                SPTRSV_BCHECK(d[k].x < G && d[k].y >= kZeroSlots && d[k].y < nslots, "fetched item", d[k].x);
                 st_slot(smem_u32(slots), d[k].y, v[k]);
                 if (ftrace != nullptr) ftrace[id[k]] = gtimer();
                 d[k] = nxt < f1 ? items[nxt] : make_int2(-1, 0);
@@ -1089,7 +1107,7 @@ __global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_const
     if (w >= wpc) {
         const int fu = blockIdx.x * wpc + (w - wpc) % wpc;   // the compute warp whose items this warp fetches
         if (!GL) fetcher<T>(a.fitems, a.fptr[fu], a.fptr[fu + 1], gm, slots, a.status, a.timeout_ns, tag,
-                          a.ftrace, (w - wpc) / wpc);
+                          a.ftrace, (w - wpc) / wpc, a.G, a.nslots);
     } else {
     const int u = blockIdx.x * wpc + w;
     const int s0 = a.unit_step0[u], n = a.unit_step0[u + 1] - s0;    // n: a multiple of UNR
@@ -1221,6 +1239,16 @@ __global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_const
                 Stage<T> S2;
                 load_stage(t + 2, S2);
                 const PubA P = pub_addr<T>(S0.pub, S0.c.w, slots_u32, gm, x);
+                if (SPTRSV_BLOCK_CHECK) {
+                    SPTRSV_BCHECK(S0.pub.x < a.nslots && (S0.pub.x < 0 || S0.pub.x >= kZeroSlots), "pub slot", S0.pub.x);
+                    SPTRSV_BCHECK(S0.pub.y < a.G, "pub mailbox", S0.pub.y);
+                    SPTRSV_BCHECK(S0.pub.z < 0 || (!CL ? false : ((S0.pub.z >> 24) < a.cs && (S0.pub.z & 0xFFFFFF) < a.nslots)), "pub remote0", S0.pub.z);
+                    SPTRSV_BCHECK(S0.pub.w < 0 || (!CL ? false : ((S0.pub.w >> 24) < a.cs && (S0.pub.w & 0xFFFFFF) < a.nslots)), "pub remote1", S0.pub.w);
+                    SPTRSV_BCHECK(S0.c.w < a.n, "row", S0.c.w);
+                    SPTRSV_BCHECK(OVF || GL || code_shfl(S0.c.x) || S0.c.x == kNoneCode || (code_kind(S0.c.x) == kKSmem && code_idx(S0.c.x) < a.nslots), "code0", S0.c.x);
+                    SPTRSV_BCHECK(OVF || GL || code_shfl(S0.c.y) || S0.c.y == kNoneCode || (code_kind(S0.c.y) == kKSmem && code_idx(S0.c.y) < a.nslots), "code1", S0.c.y);
+                    SPTRSV_BCHECK(OVF || GL || code_shfl(S0.c.z) || S0.c.z == kNoneCode || (code_kind(S0.c.z) == kKSmem && code_idx(S0.c.z) < a.nslots), "code2", S0.c.z);
+                }
                 // ---- readiness (value-as-flag; non-EXT terms hold 0) and ring waits
                 const unsigned sh = sent_hi<T>();
                 const bool pend = (hi_word(E0.e0) == sh) | (hi_word(E0.e1) == sh) | (hi_word(E0.e2) == sh);
@@ -1830,6 +1858,8 @@ sptrsv_status_t block_solve(sptrsv_handle_t h, const void *b, void *x, cudaStrea
     a.b = b;
     a.x = x;
     a.G = B.G;
+    a.n = h->n;
+    a.cs = B.cs;
     a.nslots = B.nslots;
     a.timeout_ns = h->timeout_ns;
     void *args[] = {(void *)&a};
