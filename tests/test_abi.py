@@ -97,3 +97,17 @@ def test_product_package_does_not_import_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/", ""), f
                 assert "import workloads" not in text, f
+
+
+def test_build_digest_identifies_sources_and_keys_the_traffic():
+    """The build digest (sha256 of the library sources and nvcc flags) is
+    stable, and bench.py's roofline.traffic resolves only for a matching one
+    (profiles/ncu_traffic.json is keyed by it)."""
+    import sys
+    from paper_1710_04985_b200 import build
+    d1, d2 = build.source_digest(), build.source_digest()
+    assert d1 == d2 and re.fullmatch(r"[0-9a-f]{64}", d1)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.ncu_traffic("cfg2_k_block_f64", "0" * 64) is None
+    assert bench.ncu_traffic("no_such_key", d1) is None
