@@ -151,7 +151,10 @@ __device__ __forceinline__ uint32_t bucket_of(int deps) { return deps > kTprMax 
 // prologue max(0, L0 * STAGGER_NS - STAGGER_MARGIN) ns after kernel entry, so
 // the origin tile's first records are not queued behind every warp's (0: off)
 #ifndef SPTRSV_BLOCK_STAGGER_NS
-#define SPTRSV_BLOCK_STAGGER_NS 150
+#define SPTRSV_BLOCK_STAGGER_NS 100
+#endif
+#ifndef SPTRSV_BLOCK_STAGGER_CAP
+#define SPTRSV_BLOCK_STAGGER_CAP 16000
 #endif
 #ifndef SPTRSV_BLOCK_STAGGER_MARGIN
 #define SPTRSV_BLOCK_STAGGER_MARGIN 4000
@@ -1166,7 +1169,10 @@ __global__ void __launch_bounds__(128 * (1 + kNf), 1) k_block(const __grid_const
 
         // ---- prologue
         if (SPTRSV_BLOCK_STAGGER_NS > 0) {
-            const long long d = (long long)a.unit_lev0[u] * SPTRSV_BLOCK_STAGGER_NS - SPTRSV_BLOCK_STAGGER_MARGIN;
+            // capped: the prologue burst is the first microseconds' problem, and a
+            // deep factor (a chain) must never start a warp after its wave arrived
+            const long long d = min((long long)a.unit_lev0[u] * SPTRSV_BLOCK_STAGGER_NS - SPTRSV_BLOCK_STAGGER_MARGIN,
+                                    (long long)SPTRSV_BLOCK_STAGGER_CAP);
             if (d > 0) {
                 const unsigned long long te = gtimer();
                 while (gtimer() - te < (unsigned long long)d) __nanosleep(500);
