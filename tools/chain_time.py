@@ -23,4 +23,5 @@ for _ in range(5):
     flush.fill_(1.0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); sv.solve(b, x); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
-print(f"{tag:8s} chain n={n}: {np.median(ts):.2f} ms  {sv.solve_status()}")
+inf = sv.info()
+print(f"{tag:8s} chain n={n}: {np.median(ts):.2f} ms  {sv.solve_status()}  algo {inf['algo']} blocks {inf['nblocks']} nlev {inf['nlev']}")
