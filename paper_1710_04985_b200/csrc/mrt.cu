@@ -38,6 +38,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cuda.h>
+
 #include "internal.h"
 
 namespace sptrsv {
@@ -58,6 +60,15 @@ constexpr int kRelw = SPTRSV_MRT_RELW;
 #define SPTRSV_MRT_BLOAD __ldcg      // measured: 1.656 ms vs 1.722 with __ldcs (evict-first)
 #endif
 
+// BSTAGE: the b rows of a group's first kBs positions come into shared memory
+// by TMA tile::gather4 copies issued by the loader a group ahead (the compute
+// warps copy them out at the group's start and free the buffer), the rest by
+// loads one group ahead -- fewer rows through the per-SM load path
+#ifndef SPTRSV_MRT_BSTAGE
+#define SPTRSV_MRT_BSTAGE 1
+#endif
+constexpr int kBs = SPTRSV_MRT_BSTAGE ? 64 : 0;             // staged rows per group
+static_assert(kBs % 16 == 0 && kBs <= 128, "staged rows: whole rows of every compute warp");
 constexpr int kThreadsMrt = (kCw + 1 + kRelw) * 32;        // + the loader warp (+ the release warp)
 constexpr int kRpw = kGmax / kCw;                  // rows per compute warp per group
 constexpr int kMaxDeps = 4;
@@ -70,10 +81,12 @@ template <typename T> __host__ __device__ constexpr int rec_bytes() { return siz
 // are one contiguous region: slot s of group k is at region + s rows.
 template <typename T, int CPL>
 __host__ __device__ constexpr size_t mrt_smem() {
-    return (size_t)2 * (kGmax + kHmax) * 32 * CPL * sizeof(T) + (size_t)3 * kGmax * rec_bytes<T>() + 5 * 8 + 16;
+    return (size_t)2 * (kGmax + kHmax) * 32 * CPL * sizeof(T) + (size_t)3 * kGmax * rec_bytes<T>() + 7 * 8 + 16 +
+           128 + (size_t)kBs * 32 * CPL * sizeof(T);
 }
 
-struct MrtArgs {
+struct alignas(64) MrtArgs {
+    CUtensorMap bmap;             // BSTAGE: b of this column block as a 2-D tensor {ncols (OOB: 0), n rows}
     const int32_t *gc0;           // [K+1] first group of every CTA
     const int32_t *gstart;        // [ngroups+1] first solve position of every group
     const int32_t *wptr;          // [ngroups+1] wait list of every group
@@ -127,14 +140,17 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     auto out_of = [&](int k) -> T * { return reinterpret_cast<T *>(sm + ((k & 1) ? OUT + HALO : 0u)); };
     auto halo_of = [&](int k) -> uint32_t { return smem_u32(sm) + ((k & 1) ? OUT : 2 * OUT + HALO); };
     unsigned char *meta = sm + 2 * (OUT + HALO);                                   // [3][kGmax * RB]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(meta + (size_t)3 * kGmax * RB);  // [3] records, [2] halos
-    int *nrow = reinterpret_cast<int *>(mbar + 5);                                  // [3] rows of the groups in the ring
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(meta + (size_t)3 * kGmax * RB);  // [3] records, [2] halos, bfull, bfree
+    int *nrow = reinterpret_cast<int *>(mbar + 7);                                  // [3] rows of the groups in the ring
+    T *bst = reinterpret_cast<T *>(sm + ((2 * (OUT + HALO) + (size_t)3 * kGmax * RB + 7 * 8 + 16 + 127) & ~(size_t)127));
+    uint64_t *bfull = &mbar[5], *bfree = &mbar[6];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x;
     const int g0 = a.gc0[c], ng = a.gc0[c + 1] - g0;
     const unsigned long long ep = (unsigned long long)a.epoch << 32;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 5; ++i) mbar_init(&mbar[i], 1);
+        for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);
+        mbar_init(&mbar[6], kCw);
         fence_mbar_init();
     }
     __syncthreads();
@@ -219,10 +235,32 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                 if (lane < nh) bulk_g2s_u32(hd + (uint32_t)lane * RS, x + (int64_t)m.hr * a.ld, rowbytes, hb);
             }
         };
+        // b rows of group k's first kBs positions into the staging buffer (4 rows per op)
+        auto stage_b = [&](int k) {
+            if (!kBs || k >= ng) return;
+            const int slot = k % 3;
+            mbar_wait(&mbar[slot], (uint32_t)((k / 3) & 1));
+            const int nr = min(nrow[slot], kBs), nq = (nr + 3) >> 2;
+            const unsigned char *mt = meta + (size_t)slot * kGmax * RB;
+            if (lane == 0) mbar_arrive_expect_tx(bfull, (uint32_t)nq * 4u * RS);
+            __syncwarp();
+            if (lane < nq) {
+                int r[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) r[i] = reinterpret_cast<const int32_t *>(mt + (size_t)min(4 * lane + i, nr - 1) * RB)[0];
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(bst) + (uint32_t)(4 * lane) * RS),
+                    "l"(reinterpret_cast<uint64_t>(&a.bmap)), "r"(smem_u32(bfull)), "r"(0), "r"(r[0]), "r"(r[1]),
+                    "r"(r[2]), "r"(r[3])
+                    : "memory");
+            }
+        };
         if (lane == 0) {
             issue_meta(0);
             issue_meta(1);
         }
+        stage_b(0);
         Meta mn = load_meta(1);
         prepare(0, load_meta(0));
         for (int k = 0; k <= ng; ++k) {
@@ -231,6 +269,11 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
             if (lane == 0) {
                 if (!kRelw && k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
                 issue_meta(k + 2);              // its ring slot held group k-1's records
+            }
+            if (kBs && k + 1 < ng) {            // the compute warps copied group k's staged b out: stage k + 1
+                mbar_wait(bfree, (uint32_t)(k & 1));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // their reads before the TMA writes
+                stage_b(k + 1);
             }
             prepare(k + 1, mn);                 // overlaps group k
             mn = load_meta(k + 2);
@@ -247,7 +290,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
         const int nrows = nrow[slot];
         const unsigned char *mt = meta + (size_t)slot * kGmax * RB;
 #pragma unroll
-        for (int r = 0; r < kRpw; ++r) {
+        for (int r = kBs / kCw; r < kRpw; ++r) {
             const int rr = w + r * kCw;
             const int row = rr < nrows ? reinterpret_cast<const int32_t *>(mt + (size_t)rr * RB)[0] : 0;
             const T *br = b + (int64_t)row * a.ld + lane;
@@ -260,6 +303,17 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     // register sets alternate by group parity)
     auto group = [&](int k, T (&bc)[kRpw][CPL], T (&bn)[kRpw][CPL]) {
         bar_all();                                          // barrier k
+        if (kBs) {                                          // staged b rows of this group, then free the buffer
+            mbar_wait(bfull, (uint32_t)(k & 1));
+#pragma unroll
+            for (int r = 0; r < kBs / kCw; ++r) {
+                const T *sb = bst + (size_t)(w + r * kCw) * NC + lane;
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) bc[r][j] = sb[32 * j];
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bfree)) : "memory");
+        }
         if (k + 1 < ng) load_b(k + 1, bn);                  // next group's b in flight during this one
         mbar_wait(&mbar[3 + (k & 1)], (uint32_t)((k >> 1) & 1));   // group k's halo rows
         const int nrows = nrow[k % 3];
@@ -736,6 +790,32 @@ bool mrt_eligible(sptrsv_handle_t h, const void *b, const void *x, int32_t nrhs)
            ((size_t)nrhs * h->esize) % 16 == 0;
 }
 
+// b of one column block as a 2-D tensor map for the staged rows: {nc columns,
+// n rows}, row stride ld elements, box {32 cpl columns, 1 row} (columns past
+// nc read as zero)
+using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+sptrsv_status_t encode_bmap(CUtensorMap *m, const void *bp, int n, int nc, int cpl, int64_t ld, size_t es) {
+    static EncodeTiled fn = nullptr;
+    if (fn == nullptr) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || p == nullptr)
+            return SPTRSV_ERR_CUDA;
+        fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)nc, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+    const cuuint32_t box[2] = {(cuuint32_t)(32 * cpl), 1u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = fn(m, es == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                          const_cast<void *>(bp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? SPTRSV_SUCCESS : SPTRSV_ERR_CUDA;
+}
+
 sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrhs, cudaStream_t s) {
     MrtPlan &M = h->mrt;
     if (!M.built) {
@@ -764,6 +844,10 @@ sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrh
         a.x = static_cast<char *>(x) + (size_t)c0 * es;
         a.ld = nrhs;
         a.ncols = nc;
+        if (kBs) {
+            sptrsv_status_t st = encode_bmap(&a.bmap, a.b, h->n, nc, cpl, nrhs, es);
+            if (st != SPTRSV_SUCCESS) return st;
+        }
         a.epoch = ++M.epoch;
         a.timeout_ns = h->timeout_ns;
         a.trace = static_cast<unsigned long long *>(M.trace);
