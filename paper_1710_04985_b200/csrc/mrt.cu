@@ -65,11 +65,16 @@ constexpr int kRelw = SPTRSV_MRT_RELW;
 // warps copy them out at the group's start and free the buffer), the rest by
 // loads one group ahead -- fewer rows through the per-SM load path
 #ifndef SPTRSV_MRT_BSTAGE
-#define SPTRSV_MRT_BSTAGE 1
+#define SPTRSV_MRT_BSTAGE 2
 #endif
-constexpr int kBs = SPTRSV_MRT_BSTAGE ? 64 : 0;             // staged rows per group
+constexpr int kBs = SPTRSV_MRT_BSTAGE ? 64 : 0;             // staged rows per group (per wave)
 static_assert(kBs % 16 == 0 && kBs <= 128, "staged rows: whole rows of every compute warp");
-constexpr int kThreadsMrt = (kCw + 1 + kRelw) * 32;        // + the loader warp (+ the release warp)
+// BSTAGE == 2: every b row staged, in two waves per group (positions 0..63,
+// 64..127) through the one 64-row buffer, by a stager warp of its own: wave
+// B of group k is issued when wave A was copied out, wave A of k + 1 when B was
+constexpr bool kBw2 = SPTRSV_MRT_BSTAGE == 2;
+constexpr int kThreadsBar = (kCw + 1 + kRelw) * 32;         // the group barrier: compute, loader (, release) warps
+constexpr int kThreadsMrt = kThreadsBar + (kBw2 ? 32 : 0);  // (+ the stager warp)
 constexpr int kRpw = kGmax / kCw;                  // rows per compute warp per group
 constexpr int kMaxDeps = 4;
 constexpr int kCols = 64;                          // columns per launch (column blocks of <= 64)
@@ -112,7 +117,7 @@ struct alignas(64) MrtArgs {
 // lanes reconverge first (the loader's lane-strided loops diverge)
 __device__ __forceinline__ void bar_all() {
     __syncwarp();
-    asm volatile("barrier.sync 1, %0;" ::"n"(kThreadsMrt) : "memory");
+    asm volatile("barrier.sync 1, %0;" ::"n"(kThreadsBar) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -158,6 +163,36 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     T *x = static_cast<T *>(a.x);
     const uint32_t rowbytes = (uint32_t)a.ncols * (uint32_t)sizeof(T);
 
+    if (kBw2 && w == kCw + 1 + kRelw) {
+        // ---- stager warp (BSTAGE 2): wave v = 2 k + h holds positions 64 h .. 64 h + 63 of group k
+        auto stage = [&](int v) {
+            const int k = v >> 1, lo = (v & 1) * kBs, slot = k % 3;
+            mbar_wait(&mbar[slot], (uint32_t)((k / 3) & 1));
+            const int cnt = max(0, min(nrow[slot] - lo, kBs)), nq = (cnt + 3) >> 2;
+            const unsigned char *mt = meta + (size_t)slot * kGmax * RB;
+            if (lane == 0) mbar_arrive_expect_tx(bfull, (uint32_t)nq * 4u * RS);
+            __syncwarp();
+            if (lane < nq) {
+                int r[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    r[i] = reinterpret_cast<const int32_t *>(mt + (size_t)(lo + min(4 * lane + i, cnt - 1)) * RB)[0];
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                    " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(bst) + (uint32_t)(4 * lane) * RS),
+                    "l"(reinterpret_cast<uint64_t>(&a.bmap)), "r"(smem_u32(bfull)), "r"(0), "r"(r[0]), "r"(r[1]),
+                    "r"(r[2]), "r"(r[3])
+                    : "memory");
+            }
+        };
+        if (ng > 0) stage(0);
+        for (int v = 0; v + 1 < 2 * ng; ++v) {
+            mbar_wait(bfree, (uint32_t)(v & 1));            // wave v copied out by every compute warp
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            stage(v + 1);
+        }
+        return;
+    }
     if (kRelw && w == kCw + 1) {
         // ---- release warp: progress counter after every group barrier
         for (int k = 0; k <= ng; ++k) {
@@ -260,7 +295,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
             issue_meta(0);
             issue_meta(1);
         }
-        stage_b(0);
+        if (!kBw2) stage_b(0);
         Meta mn = load_meta(1);
         prepare(0, load_meta(0));
         for (int k = 0; k <= ng; ++k) {
@@ -270,7 +305,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                 if (!kRelw && k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
                 issue_meta(k + 2);              // its ring slot held group k-1's records
             }
-            if (kBs && k + 1 < ng) {            // the compute warps copied group k's staged b out: stage k + 1
+            if (kBs && !kBw2 && k + 1 < ng) {   // the compute warps copied group k's staged b out: stage k + 1
                 mbar_wait(bfree, (uint32_t)(k & 1));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // their reads before the TMA writes
                 stage_b(k + 1);
@@ -303,18 +338,20 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     // register sets alternate by group parity)
     auto group = [&](int k, T (&bc)[kRpw][CPL], T (&bn)[kRpw][CPL]) {
         bar_all();                                          // barrier k
-        if (kBs) {                                          // staged b rows of this group, then free the buffer
-            mbar_wait(bfull, (uint32_t)(k & 1));
+        // staged b rows of wave v (rows r0 .. r0 + kBs / kCw - 1 of this warp), then free the buffer
+        auto take_wave = [&](int v, int r0) {
+            mbar_wait(bfull, (uint32_t)(v & 1));
 #pragma unroll
             for (int r = 0; r < kBs / kCw; ++r) {
                 const T *sb = bst + (size_t)(w + r * kCw) * NC + lane;
 #pragma unroll
-                for (int j = 0; j < CPL; ++j) bc[r][j] = sb[32 * j];
+                for (int j = 0; j < CPL; ++j) bc[r0 + r][j] = sb[32 * j];
             }
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bfree)) : "memory");
-        }
-        if (k + 1 < ng) load_b(k + 1, bn);                  // next group's b in flight during this one
+        };
+        if (kBs) take_wave(kBw2 ? 2 * k : k, 0);
+        if (!kBw2 && k + 1 < ng) load_b(k + 1, bn);         // next group's b in flight during this one
         mbar_wait(&mbar[3 + (k & 1)], (uint32_t)((k >> 1) & 1));   // group k's halo rows
         const int nrows = nrow[k % 3];
         const unsigned char *mt = meta + (size_t)(k % 3) * kGmax * RB;
@@ -323,6 +360,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
 #pragma unroll
         for (int r = 0; r < kRpw; ++r) {
             const int rr = w + r * kCw;
+            if (kBw2 && r == kBs / kCw) take_wave(2 * k + 1, r);   // the group's second wave
             if (rr < nrows) {
                 const unsigned char *rc = mt + (size_t)rr * RB;
                 const int4 h0 = *reinterpret_cast<const int4 *>(rc);
@@ -359,7 +397,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
             }
         }
     };
-    if (ng > 0) load_b(0, bcur);
+    if (ng > 0 && !kBw2) load_b(0, bcur);
     for (int k = 0; k < ng; k += 2) {
         group(k, bcur, bnxt);
         if (k + 1 < ng) group(k + 1, bnxt, bcur);
