@@ -65,14 +65,20 @@ constexpr int kRelw = SPTRSV_MRT_RELW;
 // warps copy them out at the group's start and free the buffer), the rest by
 // loads one group ahead -- fewer rows through the per-SM load path
 #ifndef SPTRSV_MRT_BSTAGE
-#define SPTRSV_MRT_BSTAGE 2
+#define SPTRSV_MRT_BSTAGE 3
 #endif
 constexpr int kBs = SPTRSV_MRT_BSTAGE ? 64 : 0;             // staged rows per group (per wave)
 static_assert(kBs % 16 == 0 && kBs <= 128, "staged rows: whole rows of every compute warp");
 // BSTAGE == 2: every b row staged, in two waves per group (positions 0..63,
 // 64..127) through the one 64-row buffer, by a stager warp of its own: wave
 // B of group k is issued when wave A was copied out, wave A of k + 1 when B was
-constexpr bool kBw2 = SPTRSV_MRT_BSTAGE == 2;
+constexpr bool kBw2 = SPTRSV_MRT_BSTAGE >= 2;
+// BSTAGE == 3: waves of 32 rows through two 32-row halves of the buffer (two
+// waves in flight: wave v + 2 is issued when wave v was copied out)
+constexpr int kNbuf = SPTRSV_MRT_BSTAGE == 3 ? 2 : 1;      // buffer parts
+constexpr int kWrows = kBs / kNbuf;                          // rows per wave
+constexpr int kWr = kWrows / kCw;                            // rows per compute warp per wave
+constexpr int kWaves = kGmax / kWrows;                       // waves per group (BSTAGE >= 2)
 constexpr int kThreadsBar = (kCw + 1 + kRelw) * 32;         // the group barrier: compute, loader (, release) warps
 constexpr int kThreadsMrt = kThreadsBar + (kBw2 ? 32 : 0);  // (+ the stager warp)
 constexpr int kRpw = kGmax / kCw;                  // rows per compute warp per group
@@ -86,7 +92,7 @@ template <typename T> __host__ __device__ constexpr int rec_bytes() { return siz
 // are one contiguous region: slot s of group k is at region + s rows.
 template <typename T, int CPL>
 __host__ __device__ constexpr size_t mrt_smem() {
-    return (size_t)2 * (kGmax + kHmax) * 32 * CPL * sizeof(T) + (size_t)3 * kGmax * rec_bytes<T>() + 7 * 8 + 16 +
+    return (size_t)2 * (kGmax + kHmax) * 32 * CPL * sizeof(T) + (size_t)3 * kGmax * rec_bytes<T>() + 9 * 8 + 16 +
            128 + (size_t)kBs * 32 * CPL * sizeof(T);
 }
 
@@ -145,17 +151,18 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     auto out_of = [&](int k) -> T * { return reinterpret_cast<T *>(sm + ((k & 1) ? OUT + HALO : 0u)); };
     auto halo_of = [&](int k) -> uint32_t { return smem_u32(sm) + ((k & 1) ? OUT : 2 * OUT + HALO); };
     unsigned char *meta = sm + 2 * (OUT + HALO);                                   // [3][kGmax * RB]
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(meta + (size_t)3 * kGmax * RB);  // [3] records, [2] halos, bfull, bfree
-    int *nrow = reinterpret_cast<int *>(mbar + 7);                                  // [3] rows of the groups in the ring
-    T *bst = reinterpret_cast<T *>(sm + ((2 * (OUT + HALO) + (size_t)3 * kGmax * RB + 7 * 8 + 16 + 127) & ~(size_t)127));
-    uint64_t *bfull = &mbar[5], *bfree = &mbar[6];
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(meta + (size_t)3 * kGmax * RB);  // [3] records, [2] halos, bfull[2], bfree[2]
+    int *nrow = reinterpret_cast<int *>(mbar + 9);                                  // [3] rows of the groups in the ring
+    T *bst = reinterpret_cast<T *>(sm + ((2 * (OUT + HALO) + (size_t)3 * kGmax * RB + 9 * 8 + 16 + 127) & ~(size_t)127));
+    uint64_t *bfull = &mbar[5], *bfree = &mbar[7];           // [kNbuf] each
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int c = blockIdx.x;
     const int g0 = a.gc0[c], ng = a.gc0[c + 1] - g0;
     const unsigned long long ep = (unsigned long long)a.epoch << 32;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 6; ++i) mbar_init(&mbar[i], 1);
-        mbar_init(&mbar[6], kCw);
+        for (int i = 0; i < 7; ++i) mbar_init(&mbar[i], 1);
+        mbar_init(&mbar[7], kCw);
+        mbar_init(&mbar[8], kCw);
         fence_mbar_init();
     }
     __syncthreads();
@@ -164,13 +171,14 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
     const uint32_t rowbytes = (uint32_t)a.ncols * (uint32_t)sizeof(T);
 
     if (kBw2 && w == kCw + 1 + kRelw) {
-        // ---- stager warp (BSTAGE 2): wave v = 2 k + h holds positions 64 h .. 64 h + 63 of group k
+        // ---- stager warp (BSTAGE >= 2): wave v = kWaves k + q holds positions kWrows q ..
+        // kWrows (q + 1) - 1 of group k, in buffer part v % kNbuf
         auto stage = [&](int v) {
-            const int k = v >> 1, lo = (v & 1) * kBs, slot = k % 3;
+            const int k = v / kWaves, lo = (v % kWaves) * kWrows, slot = k % 3, pb = v % kNbuf;
             mbar_wait(&mbar[slot], (uint32_t)((k / 3) & 1));
-            const int cnt = max(0, min(nrow[slot] - lo, kBs)), nq = (cnt + 3) >> 2;
+            const int cnt = max(0, min(nrow[slot] - lo, kWrows)), nq = (cnt + 3) >> 2;
             const unsigned char *mt = meta + (size_t)slot * kGmax * RB;
-            if (lane == 0) mbar_arrive_expect_tx(bfull, (uint32_t)nq * 4u * RS);
+            if (lane == 0) mbar_arrive_expect_tx(&bfull[pb], (uint32_t)nq * 4u * RS);
             __syncwarp();
             if (lane < nq) {
                 int r[4];
@@ -179,17 +187,18 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                     r[i] = reinterpret_cast<const int32_t *>(mt + (size_t)(lo + min(4 * lane + i, cnt - 1)) * RB)[0];
                 asm volatile(
                     "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-                    " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(bst) + (uint32_t)(4 * lane) * RS),
-                    "l"(reinterpret_cast<uint64_t>(&a.bmap)), "r"(smem_u32(bfull)), "r"(0), "r"(r[0]), "r"(r[1]),
+                    " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(bst) + (uint32_t)(pb * kWrows + 4 * lane) * RS),
+                    "l"(reinterpret_cast<uint64_t>(&a.bmap)), "r"(smem_u32(&bfull[pb])), "r"(0), "r"(r[0]), "r"(r[1]),
                     "r"(r[2]), "r"(r[3])
                     : "memory");
             }
         };
-        if (ng > 0) stage(0);
-        for (int v = 0; v + 1 < 2 * ng; ++v) {
-            mbar_wait(bfree, (uint32_t)(v & 1));            // wave v copied out by every compute warp
+        const int nw = kWaves * ng;
+        for (int v = 0; v < min(kNbuf, nw); ++v) stage(v);
+        for (int v = 0; v + kNbuf < nw; ++v) {
+            mbar_wait(&bfree[v % kNbuf], (uint32_t)((v / kNbuf) & 1));   // wave v copied out by every compute warp
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            stage(v + 1);
+            stage(v + kNbuf);
         }
         return;
     }
@@ -340,17 +349,21 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
         bar_all();                                          // barrier k
         // staged b rows of wave v (rows r0 .. r0 + kBs / kCw - 1 of this warp), then free the buffer
         auto take_wave = [&](int v, int r0) {
-            mbar_wait(bfull, (uint32_t)(v & 1));
+            const int pb = kBw2 ? v % kNbuf : 0;
+            const int ph = kBw2 ? (v / kNbuf) & 1 : v & 1;
+            constexpr int WR = kBw2 ? kWr : kBs / kCw;
+            mbar_wait(&bfull[pb], (uint32_t)ph);
 #pragma unroll
-            for (int r = 0; r < kBs / kCw; ++r) {
-                const T *sb = bst + (size_t)(w + r * kCw) * NC + lane;
+            for (int r = 0; r < WR; ++r) {
+                const T *sb = bst + (size_t)(pb * kWrows + w + r * kCw) * NC + lane;
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) bc[r0 + r][j] = sb[32 * j];
             }
             __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bfree)) : "memory");
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(kBw2 ? &bfree[pb] : bfree)) : "memory");
         };
-        if (kBs) take_wave(kBw2 ? 2 * k : k, 0);
+        if (kBs) take_wave(kBw2 ? kWaves * k : k, 0);
         if (!kBw2 && k + 1 < ng) load_b(k + 1, bn);         // next group's b in flight during this one
         mbar_wait(&mbar[3 + (k & 1)], (uint32_t)((k >> 1) & 1));   // group k's halo rows
         const int nrows = nrow[k % 3];
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
 #pragma unroll
         for (int r = 0; r < kRpw; ++r) {
             const int rr = w + r * kCw;
-            if (kBw2 && r == kBs / kCw) take_wave(2 * k + 1, r);   // the group's second wave
+            if (kBw2 && r > 0 && r % kWr == 0) take_wave(kWaves * k + r / kWr, r);   // the group's next wave
             if (rr < nrows) {
                 const unsigned char *rc = mt + (size_t)rr * RB;
                 const int4 h0 = *reinterpret_cast<const int4 *>(rc);
