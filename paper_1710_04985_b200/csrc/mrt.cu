@@ -73,6 +73,14 @@ static_assert(kBs % 16 == 0 && kBs <= 128, "staged rows: whole rows of every com
 // 64..127) through the one 64-row buffer, by a stager warp of its own: wave
 // B of group k is issued when wave A was copied out, wave A of k + 1 when B was
 constexpr bool kBw2 = SPTRSV_MRT_BSTAGE >= 2;
+// XTMA (needs the release warp): a group's x rows leave shared memory by TMA
+// tile::scatter4 stores issued by the release warp after the group barrier
+// (instead of the compute warps' global stores); the progress release
+// follows their completion
+#ifndef SPTRSV_MRT_XTMA
+#define SPTRSV_MRT_XTMA 1
+#endif
+constexpr bool kXtma = SPTRSV_MRT_XTMA && SPTRSV_MRT_RELW;
 // BSTAGE == 3: waves of 32 rows through two 32-row halves of the buffer (two
 // waves in flight: wave v + 2 is issued when wave v was copied out)
 constexpr int kNbuf = SPTRSV_MRT_BSTAGE == 3 ? 2 : 1;      // buffer parts
@@ -98,6 +106,7 @@ __host__ __device__ constexpr size_t mrt_smem() {
 
 struct alignas(64) MrtArgs {
     CUtensorMap bmap;             // BSTAGE: b of this column block as a 2-D tensor {ncols (OOB: 0), n rows}
+    CUtensorMap xmap;             // XTMA: x of this column block, the same shape (OOB columns not written)
     const int32_t *gc0;           // [K+1] first group of every CTA
     const int32_t *gstart;        // [ngroups+1] first solve position of every group
     const int32_t *wptr;          // [ngroups+1] wait list of every group
@@ -203,9 +212,41 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
         return;
     }
     if (kRelw && w == kCw + 1) {
-        // ---- release warp: progress counter after every group barrier
+        // ---- release warp: progress counter after every group barrier (XTMA: after the
+        // group's x rows went out by scatter4 TMA stores from its output buffer)
+        int rq[4] = {0, 0, 0, 0}, nr = 0;                  // XTMA: global rows of the group's positions 4 lane ..
+        auto rows_of = [&](int k) {
+            const int slot = k % 3;
+            mbar_wait(&mbar[slot], (uint32_t)((k / 3) & 1));
+            nr = nrow[slot];
+            const unsigned char *mt = meta + (size_t)slot * kGmax * RB;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                rq[i] = reinterpret_cast<const int32_t *>(mt + (size_t)min(4 * lane + i, max(nr - 1, 0)) * RB)[0];
+        };
         for (int k = 0; k <= ng; ++k) {
             bar_all();
+            if (kXtma && k > 0) {
+                const int nfull = nr >> 2;                 // full quadruples by TMA; the tail by this warp
+                const uint32_t src = smem_u32(out_of(k - 1)) + (uint32_t)(4 * lane) * RS;
+                if (lane < nfull)
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group"
+                                 " [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&a.xmap)),
+                                 "r"(src), "r"(0), "r"(rq[0]), "r"(rq[1]), "r"(rq[2]), "r"(rq[3])
+                                 : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                for (int p = 4 * nfull; p < nr; ++p) {     // <= 3 tail rows
+                    const int row = __shfl_sync(0xffffffffu, rq[p & 3], nfull);
+                    const T *sr = out_of(k - 1) + (size_t)p * NC;
+                    T *xr = x + (int64_t)row * a.ld;
+                    for (int j = lane; j < a.ncols; j += 32) xr[j] = sr[j];
+                }
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            // rows of the group now running, for its stores after the next barrier (its
+            // record slot is reused once that barrier passes)
+            if (kXtma && k < ng) rows_of(k);
             if (lane == 0 && k > 0) st_release_u64(a.prog + c, ep | (unsigned)k);
         }
         return;
@@ -405,10 +446,13 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
                 for (int j = 0; j < CPL; ++j) {
                     const T xi = UNIT ? acc[j] : acc[j] * di;
                     po[32 * j] = xi;
-                    if (lane + 32 * j < a.ncols) xo[32 * j] = xi;
+                    if (!kXtma && lane + 32 * j < a.ncols) xo[32 * j] = xi;
                 }
             }
         }
+        // XTMA: this warp's output rows, written by the generic proxy, are read by the
+        // release warp's TMA stores after the barrier
+        if (kXtma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     };
     if (ng > 0 && !kBw2) load_b(0, bcur);
     for (int k = 0; k < ng; k += 2) {
@@ -496,7 +540,7 @@ __global__ void k_mrt_rec(int n, const int32_t *perm, const int32_t *pos, const 
         } else {
             slot = -(j + 1);
             ++ng;
-            if (cta[j] != ci) ++nx;
+            if (cta[j] != ci || kXtma) ++nx;      // XTMA: own older groups' rows land late too
         }
         hd[2 + d] = slot;
         av[d] = tri_val[k];
@@ -529,7 +573,7 @@ __global__ void k_mrt_items(int n, int K, const int32_t *perm, const int32_t *po
         hkey[o] = (uint32_t)j;
         hitem[o] = p * kMaxDeps + d;
         ++o;
-        if (cj != ci) {
+        if (cj != ci || kXtma) {         // XTMA: also wait for this CTA's own stores of older groups
             wkey[q] = (uint32_t)gid[p] * (uint32_t)K + (uint32_t)cj;
             wneed[q] = gid[pos[j]] - gc0[cj] + 1;
             ++q;
@@ -897,6 +941,10 @@ sptrsv_status_t mrt_solve(sptrsv_handle_t h, const void *b, void *x, int32_t nrh
         a.ncols = nc;
         if (kBs) {
             sptrsv_status_t st = encode_bmap(&a.bmap, a.b, h->n, nc, cpl, nrhs, es);
+            if (st != SPTRSV_SUCCESS) return st;
+        }
+        if (kXtma) {
+            sptrsv_status_t st = encode_bmap(&a.xmap, a.x, h->n, nc, cpl, nrhs, es);
             if (st != SPTRSV_SUCCESS) return st;
         }
         a.epoch = ++M.epoch;
