@@ -81,6 +81,10 @@ constexpr bool kBw2 = SPTRSV_MRT_BSTAGE >= 2;
 #define SPTRSV_MRT_XTMA 1
 #endif
 constexpr bool kXtma = SPTRSV_MRT_XTMA && SPTRSV_MRT_RELW;
+// HALO_G4 (with XTMA's x tensor map): halo rows by tile::gather4, 4 per op
+#ifndef SPTRSV_MRT_HALO_G4
+#define SPTRSV_MRT_HALO_G4 1
+#endif
 // BSTAGE == 3: waves of 32 rows through two 32-row halves of the buffer (two
 // waves in flight: wave v + 2 is issued when wave v was copied out)
 constexpr int kNbuf = SPTRSV_MRT_BSTAGE == 3 ? 2 : 1;      // buffer parts
@@ -314,7 +318,23 @@ __global__ void __launch_bounds__(kThreadsMrt, 1) k_mrt(const __grid_constant__ 
             else asm volatile("fence.acquire.gpu;" ::: "memory");
             uint64_t *hb = &mbar[3 + (k & 1)];
             const uint32_t hd = halo_of(k);
-            {
+            if (SPTRSV_MRT_HALO_G4 && kXtma) {
+                // 4 halo rows per tile::gather4 op on the x tensor map (the last quadruple
+                // padded with its last row into unused slots; kHmax is a multiple of 4)
+                const int nq = (nh + 3) >> 2;
+                int r[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) r[i] = __shfl_sync(0xffffffffu, m.hr, max(0, min(4 * lane + i, nh - 1)) & 31);
+                if (lane == 0) mbar_arrive_expect_tx(hb, (uint32_t)nq * 4u * RS);
+                __syncwarp();
+                if (lane < nq)
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(hd + (uint32_t)(4 * lane) * RS),
+                        "l"(reinterpret_cast<uint64_t>(&a.xmap)), "r"(smem_u32(hb)), "r"(0), "r"(r[0]), "r"(r[1]),
+                        "r"(r[2]), "r"(r[3])
+                        : "memory");
+            } else {
                 if (lane == 0) mbar_arrive_expect_tx(hb, (uint32_t)nh * rowbytes);
                 __syncwarp();
                 if (lane < nh) bulk_g2s_u32(hd + (uint32_t)lane * RS, x + (int64_t)m.hr * a.ld, rowbytes, hb);
